@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the shallow-water hot path (BASELINE.json metric:
+Gcell-updates/s and HBM GB/s vs roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* is one Lax-Wendroff update of the whole grid (one launch of the
+fused sm_100a step kernel: faces + update + boundary halos).  Workload at
+N=1: BASELINE config 3, 16384^2 f32, reflective, fixed dt = 0.3 *
+stable_dt(initial state); N>1: weak scaling,
+16384^2 cells per GPU, 2-D decomposed with a one-cell halo exchange per
+step.  The 6.4 GB working set is ~50x the 126 MB L2, so no L2 flush is
+needed between steps.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_CELL = {"f32": 24, "f64": 48}      # read H,U,V + write oH,oU,oV
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index=0, period=0.02):
+        self.samples, self.reasons = [], set()
+        self.period, self.index = period, index
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _loop(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) -- only used for the cpu_baseline / --impl reference legs
+# ---------------------------------------------------------------------------
+
+def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads=None):
+    """Time the C restatement of the reference CPU path (all host threads)
+    on a bounded slab n x rows of the same workload."""
+    from oracle import c_oracle
+    from oracle import sw_oracle as so
+    threads = threads or len(os.sched_getaffinity(0))
+    H, U, V = so.init_state(n, rows, "f32")
+    dt = 0.3 * so.stable_dt(H, U, V, 1.0, 1.0)
+    a = (H, U, V)
+    b = tuple(np.empty_like(x) for x in a)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_steps and (len(times) < min_steps or time.perf_counter() - t_start < budget_s):
+        t0 = time.perf_counter()
+        c_oracle.step(*a, 1.0, 1.0, dt, out=b, threads=threads)
+        times.append(time.perf_counter() - t0)
+        a, b = b, a
+    med = statistics.median(times)
+    return {"value": n * rows / med / 1e9, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+            "sample": f"C restatement of the reference step (oracle/sw_oracle.c, DSL op order) on a "
+                      f"{n}x{rows} slab of the {n}x{n} workload, median of {len(times)} steps, "
+                      f"{threads} threads", "ms_per_step": med * 1e3}
+
+
+def numpy_sample(n, rows):
+    """The numpy restatement (single-threaded, like the reference) on a small slab."""
+    from oracle import sw_oracle as so
+    H, U, V = so.init_state(n, rows, "f32")
+    dt = 0.3 * so.stable_dt(H, U, V, 1.0, 1.0)
+    t0 = time.perf_counter()
+    so.step(H, U, V, 1.0, 1.0, dt)
+    t = time.perf_counter() - t0
+    return {"value": n * rows / t / 1e9, "cores": 1, "sample": f"numpy oracle, 1 step on {n}x{rows}"}
+
+
+# ---------------------------------------------------------------------------
+# device helpers
+# ---------------------------------------------------------------------------
+
+def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, boundary="reflective"):
+    """Gaussian-hump initial state built on the device (setup only)."""
+    import torch
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.field import DeviceField
+    from paper_1107_2157_b200.region import Extent
+    ng_x, ng_y = n_glob if n_glob else (n_x, n_y)
+    full = Extent(n_x + 2, n_y + 2)
+    H, U, V = (DeviceField(full, "f32", device, fill=0.0) for _ in range(3))
+    xs = (torch.arange(n_x, dtype=torch.float64, device=device) + x_off + 0.5) - ng_x / 2.0
+    ys = (torch.arange(n_y, dtype=torch.float64, device=device) + y_off + 0.5) - ng_y / 2.0
+    w = ng_x / 8.0
+    for r0 in range(0, n_y, 2048):          # chunk to bound f64 temporaries
+        r1 = min(n_y, r0 + 2048)
+        h = 1.0 + 0.4 * torch.exp(-(xs[None, :] ** 2 + ys[r0:r1, None] ** 2) / (w * w))
+        H.data[1 + r0:1 + r1, 1:-1] = h.to(torch.float32)
+    st = swdemo.SWState(H, U, V)
+    swdemo.apply_boundary(st, boundary)
+    return st
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=16384, help="cells per side (per GPU)")
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    n = args.n
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        rows = 1024
+        cores = len(os.sched_getaffinity(0))
+        r = cpu_port_sample(n, rows, budget_s=1e9, min_steps=args.warmup + args.steps,
+                            max_steps=args.warmup + args.steps, threads=cores)
+        line = {"metric": "Gcell-updates/s", "value": r["value"], "unit": "Gcell-updates/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
+                "config": {"workload": f"shallow-water {n}x{n} fp32 reflective, fixed dt (sampled {n}x{rows} slab)",
+                           "parallelism": "host threads"},
+                "impl": "reference",
+                "cpu_baseline": {"value": r["value"], "unit": "Gcell-updates/s", "cores": cores,
+                                 "kind": "port", "sample": r["sample"]},
+                "e2e": {"value": r["value"], "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    if world > 1:
+        from paper_1107_2157_b200 import decomp
+        return decomp.bench_main(args, rank, world)
+
+    from paper_1107_2157_b200 import _native as N
+    from paper_1107_2157_b200 import swdemo
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    st = device_gaussian_state(n, n, dev)
+    dt0 = swdemo.stable_dt(st, 1.0)
+    dt = 0.3 * dt0
+    cfg = swdemo.SWConfig(nx=n, ny=n, steps=args.steps + args.warmup, dt=dt, mode=args.mode,
+                          variant=args.variant)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+        sim.advance(args.warmup)
+        torch.cuda.synchronize()
+        # per-launch events: the step kernel is the only launch per step
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clocks:
+            torch.cuda.synchronize()
+            t_start.record(stream)
+            for k in range(args.steps):
+                ev[k].record(stream)
+                sim.advance(1)
+            ev[args.steps].record(stream)
+            t_end.record(stream)
+            torch.cuda.synchronize()
+        total_ms = t_start.elapsed_time(t_end)
+        per_launch = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    ms_step = total_ms / args.steps
+    cells = n * n
+    value = cells * args.steps / (total_ms / 1e3) / 1e9
+    avg_launch_ms = sum(per_launch) / len(per_launch)
+    bytes_launch = BYTES_PER_CELL["f32"] * cells
+    achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    fin = sim.state()
+    finite = bool(torch.isfinite(fin.H.data).all().item() and torch.isfinite(fin.U.data).all().item())
+    assert finite, "non-finite state after the timed run"
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            t = json.load(open(tp))
+            key = f"{args.mode}_{n}"
+            traffic = t.get(key)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "Gcell-updates/s (shallow-water step)", "value": round(value, 3), "unit": "Gcell-updates/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Gaussian hump h=1+0.4exp(-r^2/(n/8)^2), hu=hv=0)",
+        "config": {"workload": f"shallow-water {n}x{n} fp32, reflective, fixed dt=0.3*stable_dt (BASELINE config 3)",
+                   "mode": args.mode, "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",
+                   "l2": f"working set {6 * 4 * (n + 2) * (n + 2) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
+        "hbm_gbs": round(achieved, 1),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_source": peak_src, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": bytes_launch, "avg_launch_ms": round(avg_launch_ms, 5),
+                     "frac_of_nominal_8TBs": round(achieved / 8000.0, 4)},
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_run(n, dt, args, dev)
+    if not args.no_cpu:
+        try:
+            cb = cpu_port_sample(n, 1024)
+            cb["numpy_1core"] = numpy_sample(n, 256)
+            line["cpu_baseline"] = cb
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line))
+    return 0
+
+
+def e2e_run(n, dt, args, dev):
+    """Same metric through the public API with HOST buffers: the initial
+    state is copied from pinned host memory, ``swdemo.run`` advances it with
+    per-step fused diagnostics (mass, max|hu|, max|hv|, error word), and the
+    final state plus the per-step diagnostics come back to the host."""
+    import torch
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.field import Field
+    from paper_1107_2157_b200.region import Extent
+    steps = max(args.steps, 200)
+    st = device_gaussian_state(n, n, dev)
+    full = Extent(n + 2, n + 2)
+    pinned = []
+    for f in (st.H, st.U, st.V):
+        t = torch.empty((n + 2, n + 2), dtype=torch.float32, pin_memory=True)
+        t.copy_(f.data)
+        pinned.append(t)
+    del st
+    torch.cuda.empty_cache()
+    host_state = swdemo.SWState(*(Field(full, t.numpy(), "f32") for t in pinned))
+    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps, dt=dt, mode=args.mode, variant=args.variant)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = swdemo.run(cfg, state=host_state, to_host=True)
+    t1 = time.perf_counter()
+    state_bytes = 3 * 4 * (n + 2) * (n + 2)
+    return {"value": round(n * n * steps / (t1 - t0) / 1e9, 3), "unit": "Gcell-updates/s",
+            "h2d_bytes_per_step": round(state_bytes / steps, 1),
+            "d2h_bytes_per_step": round((state_bytes + 40 * (steps + 1)) / steps, 1),
+            "steps": steps, "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned>, to_host=True)",
+            "diagnostics": "per-step mass/max|hu|/max|hv| fused in the step kernel",
+            "final_mass": res.rows[-1][3]}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

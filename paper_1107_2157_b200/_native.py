@@ -1,0 +1,117 @@
+"""ctypes binding of the sm_100a C-ABI library ``lib/libfkc_sw.so``
+(declared in ``include/fkc_sw.h``).
+
+There is deliberately no CPU fallback: if the library is missing or fails to
+load, every entry point raises :class:`NativeUnavailable` -- the hot path is
+the CUDA kernel or nothing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libfkc_sw.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+
+FKC_OK, FKC_EDOMAIN, FKC_EUSAGE, FKC_ECUDA = 0, 1, 2, 3
+F32, F64 = 0, 1
+BC_REFLECTIVE, BC_PERIODIC, BC_NONE = 0, 1, 2
+MODE_EXACT, MODE_FAST = 0, 1
+VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA = 0, 1, 2
+ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
+
+EXPORTS = (
+    "fkc_sw_step", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
+    "fkc_region_cpy", "fkc_cshift", "fkc_halo_pack", "fkc_halo_unpack",
+    "fkc_set_tma_segment", "fkc_last_error", "fkc_abi_version",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library is not built / not loadable."""
+
+
+class FkcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[fkc rc={code}] {msg}")
+        self.code = code
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("pitch", ctypes.c_int64),
+                ("dtype", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class Reduce(ctypes.Structure):
+    _fields_ = [("mass", ctypes.c_void_p), ("max_abs_u", ctypes.c_void_p),
+                ("max_abs_v", ctypes.c_void_p), ("cfl_min", ctypes.c_void_p),
+                ("err", ctypes.c_void_p)]
+
+
+class StepArgs(ctypes.Structure):
+    _fields_ = [("grid", Grid),
+                ("H", ctypes.c_void_p), ("U", ctypes.c_void_p), ("V", ctypes.c_void_p),
+                ("oH", ctypes.c_void_p), ("oU", ctypes.c_void_p), ("oV", ctypes.c_void_p),
+                ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("dt", ctypes.c_double),
+                ("g", ctypes.c_double),
+                ("dt_bound", ctypes.c_void_p), ("cfl", ctypes.c_double),
+                ("bc", ctypes.c_int32 * 4), ("mode", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("red", Reduce)]
+
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the library in-tree with nvcc for sm_100a (see csrc/Makefile)."""
+    if force and os.path.exists(LIB_PATH):
+        os.remove(LIB_PATH)
+    subprocess.run(["make", "-s", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(f"{LIB_PATH} not built (run __graft_entry__.build() "
+                                "or `make -C paper_1107_2157_b200/csrc`)")
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover - depends on the box
+        raise NativeUnavailable(f"cannot load {LIB_PATH}: {e}") from e
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "fkc_sw_step": [ctypes.POINTER(StepArgs), vp],
+        "fkc_sw_apply_boundary": [ctypes.POINTER(Grid), vp, vp, vp, ctypes.POINTER(i32), vp],
+        "fkc_sw_reduce_state": [ctypes.POINTER(Grid), vp, vp, vp, dbl, dbl, dbl,
+                                ctypes.POINTER(Reduce), vp],
+        "fkc_sw_reduce_reset": [ctypes.POINTER(Reduce), vp],
+        "fkc_region_cpy": [i32, vp, i32, i32, i64, ctypes.POINTER(i32), vp, i64, vp],
+        "fkc_cshift": [i32, vp, i32, i32, i64, i32, i64, vp, i64, vp],
+        "fkc_halo_pack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
+        "fkc_halo_unpack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
+        "fkc_set_tma_segment": [ctypes.c_int],
+        "fkc_abi_version": [],
+        "fkc_last_error": [],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_char_p if name == "fkc_last_error" else ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc != FKC_OK:
+        msg = lib().fkc_last_error().decode(errors="replace")
+        raise FkcError(rc, msg)
+
+
+def bc_array(bc4) -> ctypes.Array:
+    return (ctypes.c_int32 * 4)(*bc4)

@@ -1,0 +1,366 @@
+// fkc_sw.cu -- C-ABI entry points (include/fkc_sw.h) over the sm_100a
+// kernels in sw_kernels.cuh.  Host code only validates arguments, encodes
+// (and caches) the TMA tensor maps and launches; it never synchronises.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/fkc_sw.h"
+#include "sw_kernels.cuh"
+
+using namespace fkc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return FKC_OK;
+}
+
+bool valid_grid(const fkc_grid* g) {
+    return g && g->nx >= 1 && g->ny >= 1 && g->pitch >= (int64_t)g->nx + 2 &&
+           (g->dtype == FKC_F32 || g->dtype == FKC_F64);
+}
+
+bool valid_bc(const int32_t* bc) {
+    for (int i = 0; i < 4; ++i)
+        if (bc[i] < FKC_BC_REFLECTIVE || bc[i] > FKC_BC_NONE) return false;
+    // periodic must be paired on an axis
+    if ((bc[0] == FKC_BC_PERIODIC) != (bc[1] == FKC_BC_PERIODIC)) return false;
+    if ((bc[2] == FKC_BC_PERIODIC) != (bc[3] == FKC_BC_PERIODIC)) return false;
+    return true;
+}
+
+BCs to_bcs(const int32_t* bc) {
+    BCs b;
+    for (int i = 0; i < 4; ++i) b.s[i] = bc[i];
+    return b;
+}
+
+RedPtrs to_red(const fkc_sw_reduce& r) {
+    RedPtrs p;
+    p.mass = r.mass;
+    p.max_u = (unsigned long long*)r.max_abs_u;
+    p.max_v = (unsigned long long*)r.max_abs_v;
+    p.cfl_min = (unsigned long long*)r.cfl_min;
+    p.err = r.err;
+    return p;
+}
+
+bool any_red(const RedPtrs& p) { return p.mass || p.max_u || p.max_v || p.cfl_min || p.err; }
+
+// ---------------------------------------------------------------------------
+// TMA tensor maps (driver entry point fetched through the runtime so the
+// library does not link libcuda directly)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    });
+    return fn;
+}
+
+struct MapKey {
+    const void* p;
+    int nx, ny;
+    int64_t pitch;
+    int boxw, boxh;
+    bool operator==(const MapKey& o) const {
+        return p == o.p && nx == o.nx && ny == o.ny && pitch == o.pitch && boxw == o.boxw && boxh == o.boxh;
+    }
+};
+
+struct MapCache {
+    static constexpr int N = 64;
+    MapKey key[N];
+    alignas(64) CUtensorMap map[N];
+    int next = 0, used = 0;
+    std::mutex mu;
+};
+MapCache g_maps;
+
+// Map over one f32 field whose element (0,0) is at `p`: tensor column t is
+// full column t-3, so box starts stay 16-B aligned when column 1 is.
+int get_map(const void* p, int nx, int ny, int64_t pitch, int boxw, CUtensorMap* out) {
+    MapKey k{p, nx, ny, pitch, boxw, tma::R};
+    std::lock_guard<std::mutex> lk(g_maps.mu);
+    for (int i = 0; i < g_maps.used; ++i)
+        if (g_maps.key[i] == k) { *out = g_maps.map[i]; return FKC_OK; }
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(FKC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    alignas(64) CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)nx + 5, (cuuint64_t)ny + 2};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    cuuint32_t box[2] = {(cuuint32_t)boxw, (cuuint32_t)tma::R};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)((const float*)p - 3), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FKC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    int slot = g_maps.next;
+    g_maps.key[slot] = k;
+    g_maps.map[slot] = m;
+    g_maps.next = (slot + 1) % MapCache::N;
+    if (g_maps.used < MapCache::N) g_maps.used++;
+    *out = m;
+    return FKC_OK;
+}
+
+bool tma_eligible(const fkc_sw_step_args* a) {
+    const fkc_grid& g = a->grid;
+    if (g.dtype != FKC_F32 || (g.nx % 4) != 0 || (g.pitch % 4) != 0) return false;
+    const void* ps[6] = {a->H, a->U, a->V, a->oH, a->oU, a->oV};
+    for (const void* p : ps)
+        if ((((uintptr_t)p) + 4) % 16 != 0) return false;
+    return true;
+}
+
+template <class T>
+int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
+    const fkc_grid& g = a->grid;
+    DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
+    RedPtrs red = to_red(a->red);
+    dim3 blk(64, 4);
+    dim3 grd((g.nx + 63) / 64, (g.ny + 3) / 4);
+    const bool fast = a->mode == FKC_MODE_FAST;
+    const bool r = any_red(red);
+#define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
+                 (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red
+    if (fast) {
+        if (r) sw_step_generic<T, true, true><<<grd, blk, 0, st>>>(GEN_ARGS);
+        else sw_step_generic<T, true, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+    } else {
+        if (r) sw_step_generic<T, false, true><<<grd, blk, 0, st>>>(GEN_ARGS);
+        else sw_step_generic<T, false, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+    }
+#undef GEN_ARGS
+    return check_launch("sw_step_generic");
+}
+
+int g_seg_override = 0;
+
+int pick_seg(int nbands, int ny) {
+    if (g_seg_override > 0) return g_seg_override;
+    // aim for >= ~8 CTAs per SM (2 resident) while keeping the 2 halo rows
+    // per segment a small fraction of the sweep
+    int seg = 256;
+    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < 148 * 8) seg /= 2;
+    return seg;
+}
+
+template <bool FAST, bool RED>
+int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
+    static bool attr_set = false;
+    auto kern = sw_step_tma<FAST, RED>;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
+        attr_set = true;
+    }
+    const fkc_grid& g = a->grid;
+    const int nbands = (g.nx + tma::BW - 1) / tma::BW;
+    const int seg = pick_seg(nbands, g.ny);
+    dim3 grd(nbands, (g.ny + seg - 1) / seg);
+    DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
+    kern<<<grd, tma::THREADS, tma::SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
+                                                     (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
+                                                     dts, (float)a->g, to_bcs(a->bc), to_red(a->red));
+    return check_launch("sw_step_tma");
+}
+
+int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
+    CUtensorMap m[6];  // main H,U,V then halo H,U,V
+    const fkc_grid& g = a->grid;
+    const void* ps[3] = {a->H, a->U, a->V};
+    int rc;
+    for (int f = 0; f < 3; ++f) {
+        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::BOXW, &m[f]))) return rc;
+        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::HALO_BOX, &m[3 + f]))) return rc;
+    }
+    const bool fast = a->mode == FKC_MODE_FAST;
+    const bool r = any_red(to_red(a->red));
+    if (fast) return r ? launch_tma_t<true, true>(a, st, m) : launch_tma_t<true, false>(a, st, m);
+    return r ? launch_tma_t<false, true>(a, st, m) : launch_tma_t<false, false>(a, st, m);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* fkc_last_error(void) { return g_err.c_str(); }
+int fkc_abi_version(void) { return FKC_ABI_VERSION; }
+
+// test hook: force the row-segment length of the TMA kernel (0 = auto)
+int fkc_set_tma_segment(int seg) {
+    if (seg < 0) return fail(FKC_EUSAGE, "segment must be >= 0");
+    g_seg_override = seg;
+    return FKC_OK;
+}
+
+int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
+    if (!a) return fail(FKC_EUSAGE, "null args");
+    if (!valid_grid(&a->grid)) return fail(FKC_EUSAGE, "invalid grid (nx=%d ny=%d pitch=%lld dtype=%d)",
+                                           a ? a->grid.nx : 0, a ? a->grid.ny : 0,
+                                           (long long)(a ? a->grid.pitch : 0), a ? a->grid.dtype : -1);
+    if (!a->H || !a->U || !a->V || !a->oH || !a->oU || !a->oV) return fail(FKC_EUSAGE, "null field pointer");
+    if (a->H == a->oH || a->U == a->oU || a->V == a->oV)
+        return fail(FKC_EUSAGE, "outputs must not alias inputs (double buffering, PAPER.md:488-493)");
+    if (!valid_bc(a->bc)) return fail(FKC_EUSAGE, "invalid boundary spec");
+    if (a->mode != FKC_MODE_EXACT && a->mode != FKC_MODE_FAST) return fail(FKC_EUSAGE, "invalid mode");
+    if (!(a->dx > 0) || !(a->dy > 0)) return fail(FKC_EUSAGE, "dx, dy must be > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    int variant = a->variant;
+    if (variant == FKC_VARIANT_AUTO) variant = tma_eligible(a) ? FKC_VARIANT_TMA : FKC_VARIANT_GENERIC;
+    if (variant == FKC_VARIANT_TMA) {
+        if (!tma_eligible(a))
+            return fail(FKC_EUSAGE, "TMA variant needs f32, nx%%4==0, pitch%%4==0 and (ptr+1) 16-B aligned");
+        return launch_tma(a, st);
+    }
+    if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");
+    return a->grid.dtype == FKC_F32 ? launch_generic<float>(a, st) : launch_generic<double>(a, st);
+}
+
+int fkc_sw_apply_boundary(const fkc_grid* g, void* H, void* U, void* V, const int32_t bc[4], void* stream) {
+    if (!valid_grid(g)) return fail(FKC_EUSAGE, "invalid grid");
+    if (!H || !U || !V) return fail(FKC_EUSAGE, "null field pointer");
+    if (!bc || !valid_bc(bc)) return fail(FKC_EUSAGE, "invalid boundary spec");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int t = 256;
+    for (int phase = 0; phase < 2; ++phase) {
+        const int n = phase == 0 ? g->ny : g->nx + 2;
+        if (g->dtype == FKC_F32)
+            sw_bc_kernel<float><<<(n + t - 1) / t, t, 0, st>>>(g->nx, g->ny, g->pitch, (float*)H, (float*)U,
+                                                               (float*)V, to_bcs(bc), phase);
+        else
+            sw_bc_kernel<double><<<(n + t - 1) / t, t, 0, st>>>(g->nx, g->ny, g->pitch, (double*)H, (double*)U,
+                                                                (double*)V, to_bcs(bc), phase);
+    }
+    return check_launch("sw_bc_kernel");
+}
+
+int fkc_sw_reduce_reset(const fkc_sw_reduce* red, void* stream) {
+    if (!red) return fail(FKC_EUSAGE, "null reduce");
+    reduce_reset_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(to_red(*red));
+    return check_launch("reduce_reset_kernel");
+}
+
+int fkc_sw_reduce_state(const fkc_grid* g, const void* H, const void* U, const void* V, double dx, double dy,
+                        double gravity, const fkc_sw_reduce* red, void* stream) {
+    if (!valid_grid(g)) return fail(FKC_EUSAGE, "invalid grid");
+    if (!H || !U || !V || !red) return fail(FKC_EUSAGE, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const double dmin = dx < dy ? dx : dy;
+    int blocks = (int)(((int64_t)g->nx * g->ny + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (g->dtype == FKC_F32)
+        sw_reduce_kernel<float><<<blocks, 256, 0, st>>>(g->nx, g->ny, g->pitch, (const float*)H, (const float*)U,
+                                                        (const float*)V, (float)gravity, (float)dmin, to_red(*red));
+    else
+        sw_reduce_kernel<double><<<blocks, 256, 0, st>>>(g->nx, g->ny, g->pitch, (const double*)H,
+                                                         (const double*)U, (const double*)V, gravity, dmin,
+                                                         to_red(*red));
+    return check_launch("sw_reduce_kernel");
+}
+
+int fkc_region_cpy(int32_t dtype, const void* src, int32_t nx_full, int32_t ny_full, int64_t src_pitch,
+                   const int32_t halo[4], void* dst, int64_t dst_pitch, void* stream) {
+    if (!src || !dst || !halo) return fail(FKC_EUSAGE, "null pointer");
+    for (int i = 0; i < 4; ++i)
+        if (halo[i] < 0) return fail(FKC_EUSAGE, "halo components must be >= 0");
+    const int mx = nx_full - halo[0] - halo[1], my = ny_full - halo[2] - halo[3];
+    if (mx < 1 || my < 1) return fail(FKC_EDOMAIN, "HaloTooLarge: halo leaves no interior");
+    if (src_pitch < nx_full || dst_pitch < mx) return fail(FKC_EUSAGE, "bad pitch");
+    dim3 b(64, 4), gr((mx + 63) / 64, (my + 3) / 4);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == FKC_F32)
+        region_cpy_kernel<float><<<gr, b, 0, st>>>((const float*)src, src_pitch, halo[0], halo[2], mx, my,
+                                                   (float*)dst, dst_pitch);
+    else if (dtype == FKC_F64)
+        region_cpy_kernel<double><<<gr, b, 0, st>>>((const double*)src, src_pitch, halo[0], halo[2], mx, my,
+                                                    (double*)dst, dst_pitch);
+    else
+        return fail(FKC_EUSAGE, "bad dtype");
+    return check_launch("region_cpy_kernel");
+}
+
+int fkc_cshift(int32_t dtype, const void* src, int32_t nx, int32_t ny, int64_t src_pitch, int32_t dim,
+               int64_t offset, void* dst, int64_t dst_pitch, void* stream) {
+    if (!src || !dst) return fail(FKC_EUSAGE, "null pointer");
+    if (nx < 1 || ny < 1 || src_pitch < nx || dst_pitch < nx) return fail(FKC_EUSAGE, "bad extent");
+    if (dim != 1 && dim != 2) return fail(FKC_EUSAGE, "dim must be 1 or 2");
+    if (src == dst) return fail(FKC_EUSAGE, "cshift is out-of-place");
+    dim3 b(64, 4), gr((nx + 63) / 64, (ny + 3) / 4);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == FKC_F32)
+        cshift_kernel<float><<<gr, b, 0, st>>>((const float*)src, src_pitch, nx, ny, dim, offset, (float*)dst,
+                                               dst_pitch);
+    else if (dtype == FKC_F64)
+        cshift_kernel<double><<<gr, b, 0, st>>>((const double*)src, src_pitch, nx, ny, dim, offset, (double*)dst,
+                                                dst_pitch);
+    else
+        return fail(FKC_EUSAGE, "bad dtype");
+    return check_launch("cshift_kernel");
+}
+
+static int halo_common(const fkc_grid* g, int side, bool unpack, const void* H, const void* U, const void* V,
+                       void* buf, void* oH, void* oU, void* oV, const void* ibuf, void* stream) {
+    if (!valid_grid(g)) return fail(FKC_EUSAGE, "invalid grid");
+    if (side < 0 || side > 3) return fail(FKC_EUSAGE, "side must be 0..3");
+    const int len = side < 2 ? g->ny : g->nx;
+    const int t = 256;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (g->dtype == FKC_F32)
+        halo_pack_kernel<float><<<(len + t - 1) / t, t, 0, st>>>(g->nx, g->ny, g->pitch, (const float*)H,
+                                                                 (const float*)U, (const float*)V, side, (float*)buf,
+                                                                 unpack, (float*)oH, (float*)oU, (float*)oV,
+                                                                 (const float*)ibuf);
+    else
+        halo_pack_kernel<double><<<(len + t - 1) / t, t, 0, st>>>(g->nx, g->ny, g->pitch, (const double*)H,
+                                                                  (const double*)U, (const double*)V, side,
+                                                                  (double*)buf, unpack, (double*)oH, (double*)oU,
+                                                                  (double*)oV, (const double*)ibuf);
+    return check_launch("halo_pack_kernel");
+}
+
+int fkc_halo_pack(const fkc_grid* g, const void* H, const void* U, const void* V, int32_t side, void* buf,
+                  void* stream) {
+    if (!H || !U || !V || !buf) return fail(FKC_EUSAGE, "null pointer");
+    return halo_common(g, side, false, H, U, V, buf, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int fkc_halo_unpack(const fkc_grid* g, void* H, void* U, void* V, int32_t side, const void* buf, void* stream) {
+    if (!H || !U || !V || !buf) return fail(FKC_EUSAGE, "null pointer");
+    return halo_common(g, side, true, nullptr, nullptr, nullptr, nullptr, H, U, V, buf, stream);
+}
+
+}  // extern "C"

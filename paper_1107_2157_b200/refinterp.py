@@ -1,0 +1,75 @@
+"""Region operators on device fields -- the ``region_cpy`` / ``region_ptr`` /
+``cshift`` API of the reference's whole-array semantics (PAPER.md:404-410,
+SPEC.md:289-306), executed by the C-ABI kernels.
+
+* :func:`region_cpy` returns a fresh device array holding the interior of
+  ``a`` selected by ``halo`` (refinterp.region_cpy_ref);
+  the source is untouched.
+* :func:`region_ptr` returns a writable strided view of that interior
+  (the pointer binding of sema.py:290-307): stores write only the Rect.
+* :func:`cshift` is the circular shift of SPEC.md:298-306:
+  ``result(x, y) = a((x + offset) mod nx, y)`` for ``dim=1``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _native as N
+from .field import DeviceField, dtype_of
+from .region import Extent, Halo, HaloTooLarge, interior_of
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _as_tensor2d(a):
+    if isinstance(a, DeviceField):
+        return a.data
+    return a
+
+
+def region_cpy(a, halo) -> "torch.Tensor":
+    """Copy of ``interior_of(a.full, halo)`` as a contiguous device tensor."""
+    torch = _torch()
+    t = _as_tensor2d(a)
+    h = Halo.of(halo)
+    ny, nx = t.shape
+    r = interior_of(Extent(nx, ny), h)            # raises HaloTooLarge
+    if t.stride(1) != 1:
+        raise ValueError("rows must be contiguous")
+    out = torch.empty((r.ny, r.nx), dtype=t.dtype, device=t.device)
+    code = 0 if t.dtype == torch.float32 else 1 if t.dtype == torch.float64 else None
+    if code is None:
+        raise ValueError(f"unsupported dtype {t.dtype}")
+    halo4 = (ctypes.c_int32 * 4)(*h)
+    N.check(N.lib().fkc_region_cpy(code, t.data_ptr(), nx, ny, t.stride(0), halo4, out.data_ptr(),
+                                   out.stride(0), torch.cuda.current_stream(t.device).cuda_stream))
+    return out
+
+
+def region_ptr(a, halo):
+    """Writable view of the interior selected by ``halo`` (no copy)."""
+    t = _as_tensor2d(a)
+    ny, nx = t.shape
+    r = interior_of(Extent(nx, ny), Halo.of(halo))
+    return t[r.y0:r.y0 + r.ny, r.x0:r.x0 + r.nx]
+
+
+def cshift(a, dim: int, offset: int) -> "torch.Tensor":
+    """Circular shift along dim 1 (x, columns) or 2 (y, rows)."""
+    torch = _torch()
+    t = _as_tensor2d(a)
+    if t.stride(1) != 1:
+        raise ValueError("rows must be contiguous")
+    ny, nx = t.shape
+    out = torch.empty((ny, nx), dtype=t.dtype, device=t.device)
+    code = 0 if t.dtype == torch.float32 else 1
+    N.check(N.lib().fkc_cshift(code, t.data_ptr(), nx, ny, t.stride(0), dim, offset, out.data_ptr(),
+                               out.stride(0), torch.cuda.current_stream(t.device).cuda_stream))
+    return out
+
+
+__all__ = ["region_cpy", "region_ptr", "cshift", "HaloTooLarge"]

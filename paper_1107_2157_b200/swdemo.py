@@ -1,0 +1,427 @@
+"""Shallow-water driver API on the B200 -- a drop-in for the reference's
+``swdemo`` module (specified in SPEC.md:472-569, absent from the shipped
+package).
+
+Same names and meaning as the reference: :class:`SWConfig`,
+:class:`SWState`, :func:`init_state`, :func:`apply_boundary`,
+:func:`stable_dt`, :func:`step_native` / :func:`advance`, :func:`run`,
+:func:`total_mass`, and the errors :class:`NonPositiveDepth` /
+:class:`NonfiniteValue`.  The engine selector of ``run``
+gains the engine ``"cuda"``; it is the only engine this package ships --
+the reference's CPU engines (``native``/``ref``/``sim``) are not
+re-implemented here, and nothing in this module computes a step on the CPU.
+
+Every numeric operation on a state runs through the C-ABI library
+(``_native``): the fused Lax-Wendroff step kernel (which also fills the
+output halo, i.e. ``apply_boundary`` of the new state, and can reduce
+CFL bound / mass / maxima of the new state in the same pass), the boundary
+kernel and the reduction kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field as dc_field
+from typing import List, Optional, Sequence, Tuple, Union
+
+import numpy as np
+
+from . import _native as N
+from .field import DeviceField, Field, dtype_of
+from .region import Extent, Halo
+
+BC_CODES = {"reflective": N.BC_REFLECTIVE, "periodic": N.BC_PERIODIC, "none": N.BC_NONE}
+MODES = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}
+VARIANTS = {"auto": N.VARIANT_AUTO, "generic": N.VARIANT_GENERIC, "tma": N.VARIANT_TMA}
+ENGINES = ("cuda",)
+
+
+class NonPositiveDepth(ValueError):
+    """h <= 0."""
+
+
+class NonfiniteValue(ArithmeticError):
+    """NaN/Inf in the state."""
+
+
+class LaunchError(ValueError):
+    """Invalid launch configuration."""
+
+
+@dataclass
+class SWConfig:
+    """SPEC.md:483-488 fields, plus the B200 engine knobs.
+
+    ``dt=None`` recomputes ``dt = stable_dt(state)`` every step (on device,
+    fused into the previous step); a number fixes dt.
+    """
+
+    nx: int = 64
+    ny: int = 64
+    dx: float = 1.0
+    dy: float = 1.0
+    g: float = 9.8
+    cfl_factor: float = 0.9
+    steps: int = 100
+    boundary: str = "reflective"
+    base: float = 1.0
+    amplitude: float = 0.4
+    center: Optional[Tuple[float, float]] = None
+    width: Optional[float] = None
+    precision: str = "f32"
+    group: Tuple[int, int] = (16, 8)
+    dt: Optional[float] = None
+    mode: str = "exact"
+    variant: str = "auto"
+
+    def __post_init__(self):
+        if not (0 < self.cfl_factor <= 1):
+            raise ValueError("cfl_factor must be in (0, 1]")
+        if self.boundary not in ("reflective", "periodic"):
+            raise ValueError(f"unknown boundary {self.boundary!r}")
+        if self.mode not in MODES:
+            raise ValueError(f"unknown mode {self.mode!r}")
+        dtype_of(self.precision)
+        Extent(self.nx, self.ny)
+
+    @property
+    def interior(self) -> Extent:
+        return Extent(self.nx, self.ny)
+
+
+AnyField = Union[Field, DeviceField]
+
+
+@dataclass
+class SWState:
+    """H (h), U (hu), V (hv) sharing one full extent, halo [1,1,1,1]."""
+
+    H: AnyField
+    U: AnyField
+    V: AnyField
+    g: float = 9.8
+    dx: float = 1.0
+    dy: float = 1.0
+    t: float = 0.0
+
+    @property
+    def on_device(self) -> bool:
+        return isinstance(self.H, DeviceField)
+
+    @property
+    def full(self) -> Extent:
+        return self.H.full
+
+    @property
+    def precision(self) -> str:
+        return self.H.precision
+
+    def to_device(self, device=None) -> "SWState":
+        if self.on_device:
+            return self
+        return SWState(*(DeviceField.from_field(f, device) for f in (self.H, self.U, self.V)),
+                       self.g, self.dx, self.dy, self.t)
+
+    def to_host(self) -> "SWState":
+        if not self.on_device:
+            return self
+        return SWState(self.H.to_field(), self.U.to_field(), self.V.to_field(),
+                       self.g, self.dx, self.dy, self.t)
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _grid(f: DeviceField) -> N.Grid:
+    return N.Grid(f.full.nx - 2, f.full.ny - 2, f.pitch, f.dtype_code, 0)
+
+
+def _bc4(boundary: Union[str, Sequence[str]]) -> Tuple[int, int, int, int]:
+    if isinstance(boundary, str):
+        return (BC_CODES[boundary],) * 4
+    return tuple(BC_CODES[b] for b in boundary)
+
+
+def _as_device(state: SWState) -> SWState:
+    if not state.on_device:
+        return state.to_device()
+    return state
+
+
+class ReductionSlots:
+    """Device slots for the fused reductions: one row of 5 x 64-bit words
+    per state: [mass (f64), max|hu| (f64 bits), max|hv| (f64 bits),
+    min CFL bound (f64 bits), error word]."""
+
+    INF_BITS = 0x7FF0000000000000
+
+    def __init__(self, n: int, device):
+        torch = _torch()
+        self.n = n
+        self.buf = torch.zeros((n, 5), dtype=torch.int64, device=device)
+        self.template = torch.tensor([0, 0, 0, self.INF_BITS, 0], dtype=torch.int64, device=device)
+        self.reset()
+
+    def reset(self, lo: int = 0, hi: Optional[int] = None):
+        hi = self.n if hi is None else hi
+        self.buf[lo:hi].copy_(self.template.expand(hi - lo, 5))
+
+    def addr(self, i: int, k: int) -> int:
+        return self.buf.data_ptr() + (i * 5 + k) * 8
+
+    def reduce_struct(self, i: int, mass=True, maxima=True, cfl=True, err=True) -> N.Reduce:
+        return N.Reduce(self.addr(i, 0) if mass else None,
+                        self.addr(i, 1) if maxima else None,
+                        self.addr(i, 2) if maxima else None,
+                        self.addr(i, 3) if cfl else None,
+                        self.addr(i, 4) if err else None)
+
+    @staticmethod
+    def decode(rows_i64: np.ndarray):
+        r = np.ascontiguousarray(rows_i64)
+        as_f = r.view(np.float64)
+        return {"mass": as_f[:, 0].copy(), "max_hu": as_f[:, 1].copy(), "max_hv": as_f[:, 2].copy(),
+                "cfl_min": as_f[:, 3].copy(), "err": r[:, 4].astype(np.uint32)}
+
+
+def raise_for_error(err_word: int, where: str = ""):
+    if err_word & N.ERR_WATCHDOG:
+        raise RuntimeError(f"device watchdog fired {where}")
+    if err_word & N.ERR_NONFINITE:
+        raise NonfiniteValue(f"non-finite state {where}")
+    if err_word & N.ERR_NONPOSITIVE_DEPTH:
+        raise NonPositiveDepth(f"depth <= 0 {where}")
+
+
+# ---------------------------------------------------------------------------
+# reference API
+# ---------------------------------------------------------------------------
+
+def init_state(cfg: SWConfig, device=None) -> SWState:
+    """Gaussian hump ``h = base + amp*exp(-r^2/width^2)`` at cell centres,
+    hu = hv = 0, evaluated in f64 and rounded to the
+    precision, uploaded, halos filled on device.  ``device=None`` keeps
+    the state on the current CUDA device."""
+    nx, ny = cfg.nx, cfg.ny
+    cx, cy = cfg.center if cfg.center is not None else (nx * cfg.dx / 2.0, ny * cfg.dy / 2.0)
+    w = cfg.width if cfg.width is not None else nx * cfg.dx / 8.0
+    xc = (np.arange(nx, dtype=np.float64) + 0.5) * cfg.dx - cx
+    yc = (np.arange(ny, dtype=np.float64) + 0.5) * cfg.dy - cy
+    h = cfg.base + cfg.amplitude * np.exp(-(xc[None, :] ** 2 + yc[:, None] ** 2) / (w * w))
+    full = Extent(nx + 2, ny + 2)
+    dt_ = dtype_of(cfg.precision)
+    H = Field.zeros(full, cfg.precision)
+    H.data[1:-1, 1:-1] = h.astype(dt_)
+    st = SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
+                 cfg.g, cfg.dx, cfg.dy, 0.0).to_device(device)
+    apply_boundary(st, cfg.boundary)
+    return st
+
+
+def apply_boundary(state: SWState, mode: Union[str, Sequence[str]] = "reflective", stream=None) -> SWState:
+    """Fill the one-cell halo in place, on device."""
+    if not state.on_device:
+        dev = _as_device(state)
+        apply_boundary(dev, mode, stream)
+        for name in ("H", "U", "V"):
+            getattr(state, name).data[...] = getattr(dev, name).to_numpy()
+        return state
+    g = _grid(state.H)
+    bc = N.bc_array(_bc4(mode))
+    N.check(N.lib().fkc_sw_apply_boundary(ctypes.byref(g), state.H.ptr, state.U.ptr, state.V.ptr, bc,
+                                          _stream_ptr(stream)))
+    return state
+
+
+def reduce_state(state: SWState, stream=None) -> dict:
+    """mass, max|hu|, max|hv|, min CFL bound and error word of a state
+    (one fused device reduction)."""
+    st = _as_device(state)
+    slots = ReductionSlots(1, st.H.storage.device)
+    red = slots.reduce_struct(0)
+    g = _grid(st.H)
+    N.check(N.lib().fkc_sw_reduce_state(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, st.dx, st.dy, st.g,
+                                        ctypes.byref(red), _stream_ptr(stream)))
+    d = ReductionSlots.decode(slots.buf.cpu().numpy())
+    return {k: v[0] for k, v in d.items()}
+
+
+def stable_dt(state: SWState, cfl_factor: float = 1.0) -> float:
+    """dt = cfl * min over interior of min(dx,dy)/(sqrt(g h) + max(|hu|,|hv|)/h)
+    (SPEC.md:508-516), computed in field precision on device."""
+    r = reduce_state(state)
+    raise_for_error(int(r["err"]), "in stable_dt")
+    f = dtype_of(state.precision).type
+    return float(f(cfl_factor) * f(r["cfl_min"]))
+
+
+def total_mass(state: SWState) -> float:
+    """Sum of interior h * dx * dy."""
+    return float(reduce_state(state)["mass"]) * state.dx * state.dy
+
+
+def _step_args(src: SWState, dst: SWState, dt: float, boundary, mode: str, variant: str,
+               red: Optional[N.Reduce] = None, dt_bound: Optional[int] = None, cfl: float = 1.0) -> N.StepArgs:
+    a = N.StepArgs()
+    a.grid = _grid(src.H)
+    a.H, a.U, a.V = src.H.ptr, src.U.ptr, src.V.ptr
+    a.oH, a.oU, a.oV = dst.H.ptr, dst.U.ptr, dst.V.ptr
+    a.dx, a.dy, a.dt, a.g = src.dx, src.dy, float(dt), src.g
+    a.dt_bound = dt_bound
+    a.cfl = cfl
+    a.bc = N.bc_array(_bc4(boundary))
+    a.mode = MODES[mode]
+    a.variant = VARIANTS[variant]
+    if red is not None:
+        a.red = red
+    return a
+
+
+def advance(state: SWState, dt: float, boundary="reflective", mode: str = "exact",
+            variant: str = "auto", out: Optional[SWState] = None, stream=None) -> SWState:
+    """Engine contract ``advance(state, dt) -> state``: one
+    Lax-Wendroff step into fresh (or given) buffers; the input state is never
+    mutated.  The output halo is filled per ``boundary``
+    in the same kernel (== apply_boundary of the new state)."""
+    host = not state.on_device
+    src = _as_device(state)
+    if out is None:
+        out = SWState(src.H.empty_like(), src.U.empty_like(), src.V.empty_like(), src.g, src.dx, src.dy, src.t)
+    a = _step_args(src, out, dt, boundary, mode, variant)
+    N.check(N.lib().fkc_sw_step(ctypes.byref(a), _stream_ptr(stream)))
+    out.t = src.t + float(dt)
+    return out.to_host() if host else out
+
+
+def step_native(state: SWState, dt: float, boundary="reflective", mode: str = "exact") -> SWState:
+    """Name-compatible alias of the reference's ``step_native``
+    -- executed by the CUDA kernel."""
+    return advance(state, dt, boundary, mode)
+
+
+# ---------------------------------------------------------------------------
+# device-resident time loop
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RunResult:
+    rows: List[Tuple[int, float, float, float, float, float]]  # step,t,dt,mass,max_hu,max_hv
+    state: SWState
+    dts: np.ndarray = dc_field(default_factory=lambda: np.zeros(0))
+
+
+class Simulation:
+    """Double-buffered device state + per-step fused reductions.
+
+    ``advance(n)`` enqueues n steps on the stream without any host
+    synchronisation: with ``cfg.dt is None`` each step reads its dt bound
+    from the reduction slot the previous step (or the initial reduction)
+    wrote, exactly like ``run`` recomputes ``stable_dt`` every step
+    (SPEC.md:529-537).
+    """
+
+    def __init__(self, cfg: SWConfig, state: Optional[SWState] = None, diagnostics: bool = True,
+                 capacity: Optional[int] = None, stream=None, boundary=None):
+        torch = _torch()
+        self.cfg = cfg
+        self.stream = stream
+        self.boundary = boundary if boundary is not None else cfg.boundary
+        st = state if state is not None else init_state(cfg)
+        st = _as_device(st)
+        self.a = st
+        self.b = SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx, st.dy, st.t)
+        self.diag = diagnostics or cfg.dt is None
+        self.n = 0
+        cap = (capacity if capacity is not None else cfg.steps) + 1
+        self.slots = ReductionSlots(cap, st.H.storage.device) if self.diag else None
+        if self.diag:
+            red = self.slots.reduce_struct(0)
+            g = _grid(st.H)
+            N.check(N.lib().fkc_sw_reduce_state(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, st.dx, st.dy,
+                                                st.g, ctypes.byref(red), _stream_ptr(stream)))
+        self._args = [None, None]
+        self.torch = torch
+
+    def _args_for(self, i: int) -> N.StepArgs:
+        src, dst = (self.a, self.b) if i % 2 == 0 else (self.b, self.a)
+        cfg = self.cfg
+        red = self.slots.reduce_struct(i + 1) if self.diag else None
+        bound = self.slots.addr(i, 3) if cfg.dt is None else None
+        return _step_args(src, dst, cfg.dt if cfg.dt is not None else 0.0, self.boundary, cfg.mode,
+                          cfg.variant, red, bound, cfg.cfl_factor)
+
+    def advance(self, steps: int):
+        if self.diag and self.n + steps >= self.slots.n:
+            raise ValueError("reduction slot capacity exceeded")
+        L = N.lib()
+        sp = _stream_ptr(self.stream)
+        for _ in range(steps):
+            a = self._args_for(self.n)
+            N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+            self.n += 1
+        return self
+
+    def state(self) -> SWState:
+        s = self.a if self.n % 2 == 0 else self.b
+        return s
+
+    def diagnostics(self) -> dict:
+        """One device->host copy of all reduction slots so far."""
+        if not self.diag:
+            return {}
+        return ReductionSlots.decode(self.slots.buf[: self.n + 1].cpu().numpy())
+
+    def rows(self) -> RunResult:
+        d = self.diagnostics()
+        cfg = self.cfg
+        f = dtype_of(cfg.precision).type
+        rows = []
+        dts = []
+        t = 0.0
+        if d["err"][0]:
+            raise_for_error(int(d["err"][0]), "in the initial state")
+        for k in range(self.n):
+            if d["err"][k + 1]:
+                raise_for_error(int(d["err"][k + 1]), f"at step {k + 1}")
+            dt = float(cfg.dt) if cfg.dt is not None else float(f(cfg.cfl_factor) * f(d["cfl_min"][k]))
+            t += dt
+            dts.append(dt)
+            rows.append((k + 1, t, dt, float(d["mass"][k + 1]) * cfg.dx * cfg.dy,
+                         float(d["max_hu"][k + 1]), float(d["max_hv"][k + 1])))
+        st = self.state()
+        st.t = t
+        return RunResult(rows, st, np.array(dts))
+
+
+def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
+        to_host: bool = False) -> RunResult:
+    """Time loop: apply_boundary -> dt -> advance -> swap ->
+    diagnostics (mass, max|hu|, max|hv|, dt), aborting on non-finite values.
+
+    The whole loop is enqueued on the GPU; per-step diagnostics come from the
+    reductions fused into each step and are read back once at the end.
+    A host ``state`` is uploaded first; ``to_host=True`` returns the final
+    state as host Fields.
+    """
+    if engine not in ENGINES:
+        raise ValueError(f"engine {engine!r} is not provided by the B200 package "
+                         f"(available: {ENGINES}); the CPU engines live in the reference")
+    sim = Simulation(cfg, state=state, diagnostics=True)
+    sim.advance(cfg.steps)
+    res = sim.rows()
+    if to_host:
+        res.state = res.state.to_host()
+    return res

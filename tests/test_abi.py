@@ -1,0 +1,81 @@
+"""CPU tier: the C-ABI library builds, loads and exports exactly what
+include/fkc_sw.h declares, and the ctypes mirrors match the C struct layout."""
+
+import ctypes
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+from paper_1107_2157_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fkc_sw.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fkc_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = N.lib()
+    names = declared_functions()
+    assert set(names) == set(N.EXPORTS), (names, N.EXPORTS)
+    for name in names:
+        assert hasattr(L, name), name
+    assert L.fkc_abi_version() == 1
+
+
+def test_usage_errors_without_gpu():
+    L = N.lib()
+    # null args -> usage error, message set, no device touched
+    assert L.fkc_sw_step(None, None) == N.FKC_EUSAGE
+    assert b"null" in L.fkc_last_error()
+    a = N.StepArgs()
+    a.grid = N.Grid(0, 4, 8, 0, 0)
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    a.grid = N.Grid(8, 8, 12, 0, 0)
+    a.H = a.U = a.V = a.oH = a.oU = a.oV = 1024
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE   # aliasing
+    halo = (ctypes.c_int32 * 4)(3, 3, 0, 0)
+    assert L.fkc_region_cpy(0, 16, 5, 5, 5, halo, 32, 5, None) == N.FKC_EDOMAIN  # HaloTooLarge
+    assert L.fkc_set_tma_segment(-1) == N.FKC_EUSAGE
+
+
+def test_struct_layout_matches_header():
+    probe = r"""
+    #include <stdio.h>
+    #include <stddef.h>
+    #include "fkc_sw.h"
+    int main(void) {
+      printf("%zu %zu %zu\n", sizeof(fkc_grid), sizeof(fkc_sw_reduce), sizeof(fkc_sw_step_args));
+      printf("%zu %zu %zu %zu %zu %zu\n", offsetof(fkc_sw_step_args, H), offsetof(fkc_sw_step_args, dx),
+             offsetof(fkc_sw_step_args, dt_bound), offsetof(fkc_sw_step_args, bc),
+             offsetof(fkc_sw_step_args, variant), offsetof(fkc_sw_step_args, red));
+      return 0;
+    }
+    """
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "p.c")
+        open(c, "w").write(probe)
+        exe = os.path.join(d, "p")
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()
+    got = list(map(int, out))
+    S = N.StepArgs
+    want = [ctypes.sizeof(N.Grid), ctypes.sizeof(N.Reduce), ctypes.sizeof(S),
+            S.H.offset, S.dx.offset, S.dt_bound.offset, S.bc.offset, S.variant.offset, S.red.offset]
+    assert got == want
+
+
+def test_sm100a_sass_present():
+    """The shipped .so carries sm_100a SASS (no PTX-JIT dependence)."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
