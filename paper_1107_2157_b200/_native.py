@@ -26,7 +26,7 @@ ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
 EXPORTS = (
     "fkc_sw_step", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_halo_pack", "fkc_halo_unpack",
-    "fkc_set_tma_segment", "fkc_last_error", "fkc_abi_version",
+    "fkc_set_tma_segment", "fkc_test_div_f32", "fkc_last_error", "fkc_abi_version",
 )
 
 
@@ -96,6 +96,7 @@ def lib():
         "fkc_halo_pack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
         "fkc_halo_unpack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
         "fkc_set_tma_segment": [ctypes.c_int],
+        "fkc_test_div_f32": [vp, vp, vp, vp, i64, vp],
         "fkc_abi_version": [],
         "fkc_last_error": [],
     }

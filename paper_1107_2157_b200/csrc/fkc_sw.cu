@@ -155,11 +155,11 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
 #define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
                  (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red
     if (fast) {
-        if (r) sw_step_generic<T, true, true><<<grd, blk, 0, st>>>(GEN_ARGS);
-        else sw_step_generic<T, true, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+        if (r) sw_step_generic<T, DIV_FAST, true><<<grd, blk, 0, st>>>(GEN_ARGS);
+        else sw_step_generic<T, DIV_FAST, false><<<grd, blk, 0, st>>>(GEN_ARGS);
     } else {
-        if (r) sw_step_generic<T, false, true><<<grd, blk, 0, st>>>(GEN_ARGS);
-        else sw_step_generic<T, false, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+        if (r) sw_step_generic<T, DIV_IEEE, true><<<grd, blk, 0, st>>>(GEN_ARGS);
+        else sw_step_generic<T, DIV_IEEE, false><<<grd, blk, 0, st>>>(GEN_ARGS);
     }
 #undef GEN_ARGS
     return check_launch("sw_step_generic");
@@ -185,24 +185,24 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
         attr_set = true;
     }
     const fkc_grid& g = a->grid;
-    const int nbands = (g.nx + tma::BW - 1) / tma::BW;
+    const int nstrips = (g.nx + tma::OWN - 1) / tma::OWN;
+    const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
     const int seg = pick_seg(nbands, g.ny);
     dim3 grd(nbands, (g.ny + seg - 1) / seg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, tma::SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
+    kern<<<grd, tma::THREADS, tma::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
                                                      (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
                                                      dts, (float)a->g, to_bcs(a->bc), to_red(a->red));
     return check_launch("sw_step_tma");
 }
 
 int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
-    CUtensorMap m[6];  // main H,U,V then halo H,U,V
+    CUtensorMap m[3];  // H, U, V
     const fkc_grid& g = a->grid;
     const void* ps[3] = {a->H, a->U, a->V};
     int rc;
     for (int f = 0; f < 3; ++f) {
         if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::BOXW, &m[f]))) return rc;
-        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::HALO_BOX, &m[3 + f]))) return rc;
     }
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(to_red(a->red));
@@ -225,6 +225,12 @@ int fkc_set_tma_segment(int seg) {
     if (seg < 0) return fail(FKC_EUSAGE, "segment must be >= 0");
     g_seg_override = seg;
     return FKC_OK;
+}
+
+int fkc_test_div_f32(const float* a, const float* b, float* q, float* qref, int64_t n, void* stream) {
+    if (!a || !b || !q || !qref || n < 0) return fail(FKC_EUSAGE, "bad arguments");
+    test_div_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, b, q, qref, n);
+    return check_launch("test_div_kernel");
 }
 
 int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
