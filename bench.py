@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--n", type=int, default=16384, help="cells per side (per GPU)")
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
+    ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -208,6 +209,8 @@ def main():
 
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
+    if args.seg:
+        N.check(N.lib().fkc_set_tma_segment(args.seg))
     st = device_gaussian_state(n, n, dev)
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0

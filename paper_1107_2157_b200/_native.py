@@ -13,7 +13,7 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libfkc_sw.so")
+LIB_PATH = os.environ.get("FKC_LIB") or os.path.join(PKG_DIR, "lib", "libfkc_sw.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 FKC_OK, FKC_EDOMAIN, FKC_EUSAGE, FKC_ECUDA = 0, 1, 2, 3

@@ -11,7 +11,7 @@
 #include <string>
 
 #include "../../include/fkc_sw.h"
-#include "sw_kernels.cuh"
+#include "sw_tma.cuh"
 
 using namespace fkc;
 
@@ -167,48 +167,51 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
 
 int g_seg_override = 0;
 
-int pick_seg(int nbands, int ny) {
+int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
-    // aim for >= ~8 CTAs per SM (2 resident) while keeping the 2 halo rows
-    // per segment a small fraction of the sweep
+    // >= ~4 waves of resident CTAs, while keeping the 2 halo rows per
+    // segment a small fraction of the sweep
     int seg = 256;
-    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < 148 * 8) seg /= 2;
+    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < (int64_t)148 * ctas_per_sm * 4) seg /= 2;
     return seg;
 }
 
-template <bool FAST, bool RED>
+template <int CPL, bool FAST, bool RED>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
+    using G = tma::Geo<CPL>;
     static bool attr_set = false;
-    auto kern = sw_step_tma<FAST, RED>;
+    auto kern = sw_step_tma<CPL, FAST, RED>;
     if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tma::SMEM_BYTES);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
         attr_set = true;
     }
     const fkc_grid& g = a->grid;
-    const int nstrips = (g.nx + tma::OWN - 1) / tma::OWN;
+    const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
     const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
-    const int seg = pick_seg(nbands, g.ny);
+    const int seg = pick_seg(nbands, g.ny, G::CTAS_PER_SM);
     dim3 grd(nbands, (g.ny + seg - 1) / seg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, tma::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
-                                                     (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
-                                                     dts, (float)a->g, to_bcs(a->bc), to_red(a->red));
+    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
+                                                   (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
+                                                   dts, (float)a->g, to_bcs(a->bc), to_red(a->red));
     return check_launch("sw_step_tma");
 }
 
-int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
+template <int CPL>
+int launch_tma_cpl(const fkc_sw_step_args* a, cudaStream_t st) {
     CUtensorMap m[3];  // H, U, V
     const fkc_grid& g = a->grid;
     const void* ps[3] = {a->H, a->U, a->V};
     int rc;
-    for (int f = 0; f < 3; ++f) {
-        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::BOXW, &m[f]))) return rc;
-    }
+    for (int f = 0; f < 3; ++f)
+        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<CPL>::LOAD, &m[f]))) return rc;
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(to_red(a->red));
-    if (fast) return r ? launch_tma_t<true, true>(a, st, m) : launch_tma_t<true, false>(a, st, m);
-    return r ? launch_tma_t<false, true>(a, st, m) : launch_tma_t<false, false>(a, st, m);
+    if (fast) return r ? launch_tma_t<CPL, true, true>(a, st, m) : launch_tma_t<CPL, true, false>(a, st, m);
+    return r ? launch_tma_t<CPL, false, true>(a, st, m) : launch_tma_t<CPL, false, false>(a, st, m);
 }
+
+int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) { return launch_tma_cpl<4>(a, st); }
 
 }  // namespace
 

@@ -1,0 +1,327 @@
+// sw_tma.cuh -- the product kernel: per-warp TMA y-sweep of the fused
+// two-step Lax-Wendroff step (f32).
+//
+// Geometry.  A warp owns a strip of OWN = 30*CPL columns and `seg` rows.
+// It loads LOAD = 32*CPL columns (the strip plus CPL columns on each side):
+// lane l holds CPL consecutive cells of every row; lanes 0 and 31 are
+// "ghost" lanes whose cells lie outside the strip -- they exist so that
+// every x-face an owned lane (1..30) needs is produced in SIMD by a
+// neighbouring lane (no divergent edge work, no separate halo loads).
+//
+// Pipeline.  Lane 0 streams the strip's rows of H, U, V through a private
+// S-stage shared-memory ring (R rows per stage, one cp.async.bulk.tensor box
+// per field, completion on an mbarrier with expect_tx); the warp never waits
+// for another warp.  Each row is read once from shared memory (one vector
+// LDS per field), its cell quantities (fxu, cross) are computed once, the
+// y-face below it is carried in registers from the previous row, the x-face
+// right of lane's last cell uses lane+1's first cell (shfl.down) and the face
+// left of its first cell is lane-1's last face (shfl.up).  The row above is
+// then updated and stored with vector stores; the output halo (boundary
+// conditions) and optional reductions are emitted in the same pass.
+#pragma once
+#include "sw_kernels.cuh"
+
+namespace fkc {
+namespace tma {
+constexpr int WARPS = 4;                 // warps (strips) per CTA
+constexpr int R = 4;                     // rows per stage
+constexpr int S = 4;                     // ring stages per warp
+template <int CPL> struct Geo {
+    static constexpr int LOAD = 32 * CPL;                 // columns loaded per strip
+    static constexpr int OWN = 30 * CPL;                  // columns owned per strip
+    static constexpr int FIELD_BYTES = R * LOAD * 4;
+    static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
+    static constexpr int WARP_RING = S * STAGE_BYTES;
+    static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
+    static constexpr int CTAS_PER_SM = CPL == 4 ? 2 : 4;   // register budget: 255 / 128 regs
+    static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
+};
+constexpr int THREADS = WARPS * 32;
+#ifndef FKC_EXACT_ALWAYS_FIXUP
+#define FKC_EXACT_ALWAYS_FIXUP 0
+#endif
+#ifndef FKC_EXACT_UNROLL
+#define FKC_EXACT_UNROLL 1
+#endif
+}  // namespace tma
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(b), "r"(parity) : "memory");
+    return ok != 0;
+}
+// Bounded wait: a lost TMA transaction (a bug, never expected) sets the
+// watchdog bit and traps after ~2 s instead of hanging the GPU.
+__device__ __noinline__ void watchdog_fire(uint32_t* err) {
+    atomicOr(err ? err : &g_watchdog_flag, 4u);
+    __threadfence_system();
+    asm volatile("trap;");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity, uint32_t* err) {
+    if (mbar_try_wait(b, parity)) return;
+    const long long t0 = clock64();
+    for (uint32_t spins = 1;; ++spins) {
+        if (mbar_try_wait(b, parity)) return;
+        if ((spins & 255u) == 0 && clock64() - t0 > 4000000000ll) watchdog_fire(err);
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];"
+        :: "r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+
+// CPL consecutive floats: shared-memory load, global store.
+template <int CPL> struct VecF {
+    float v[CPL];
+};
+template <int CPL>
+__device__ __forceinline__ VecF<CPL> lds_vec(uint32_t a) {
+    VecF<CPL> r;
+    if constexpr (CPL == 4)
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(a));
+    else
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.v[0]), "=f"(r.v[1]) : "r"(a));
+    return r;
+}
+template <int CPL>
+__device__ __forceinline__ void stg_vec(float* p, const float (&v)[CPL], float sgn = 1.0f) {
+    if constexpr (CPL == 4)
+        *(float4*)p = make_float4(sgn * v[0], sgn * v[1], sgn * v[2], sgn * v[3]);
+    else
+        *(float2*)p = make_float2(sgn * v[0], sgn * v[1]);
+}
+
+// One stage = R rows x LOAD columns of H, U, V (3 boxes), completing on `bar`.
+template <int CPL>
+__device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUtensorMap* mH,
+                                            const CUtensorMap* mU, const CUtensorMap* mV, int tx, int ty) {
+    constexpr int FB = tma::Geo<CPL>::FIELD_BYTES;
+    mbar_expect_tx(bar, tma::Geo<CPL>::STAGE_BYTES);
+    tma_load_2d(st, mH, tx, ty, bar);
+    tma_load_2d(st + FB, mU, tx, ty, bar);
+    tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
+}
+
+// Faces of one freshly loaded row: cell quantities nc, the y-faces between
+// the previous row pc and this row (if have_prev), and the x-faces of this
+// row (if want_x): nxr[i] = face between cell i and i+1 of the lane (cell
+// CPL comes from lane+1), nxl = face left of cell 0 (= nxr[CPL-1] of lane-1).
+template <int DM, int CPL>
+__device__ __forceinline__ void row_faces(const VecF<CPL>& h, const VecF<CPL>& u, const VecF<CPL>& v,
+                                          const CellQ<float> (&pc)[CPL], bool have_prev, bool want_x,
+                                          const Coef<float>& c, CellQ<float> (&nc)[CPL],
+                                          FaceF<float> (&yup)[CPL], FaceF<float> (&nxr)[CPL],
+                                          FaceF<float>& nxl, bool& ok) {
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) nc[i] = cell_q<float, DM>(h.v[i], u.v[i], v.v[i], c, ok);
+    if (have_prev) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) yup[i] = y_face<float, DM>(pc[i], nc[i], c, ok);
+    }
+    if (want_x) {
+        CellQ<float> nb;  // first cell of lane+1
+        nb.h = __shfl_down_sync(0xffffffffu, nc[0].h, 1);
+        nb.u = __shfl_down_sync(0xffffffffu, nc[0].u, 1);
+        nb.v = __shfl_down_sync(0xffffffffu, nc[0].v, 1);
+        nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu, 1);
+        nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr, 1);
+        nb.fv = 0.f;
+#pragma unroll
+        for (int i = 0; i < CPL - 1; ++i) nxr[i] = x_face<float, DM>(nc[i], nc[i + 1], c, ok);
+        nxr[CPL - 1] = x_face<float, DM>(nc[CPL - 1], nb, c, ok);
+        nxl.fh = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fh, 1);
+        nxl.fu = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fu, 1);
+        nxl.fv = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fv, 1);
+    }
+}
+
+// Tensor coordinates: the maps are encoded with base = &field(-3, 0) so that
+// full-array column x is tensor column x + 3 (16-B aligned boxes).  Strip j
+// owns columns [1 + OWN j, OWN (j+1)] and loads full columns
+// [1 + OWN j - CPL, OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
+template <int CPL, bool FAST, bool RED>
+__global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::CTAS_PER_SM)
+sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
+            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg,
+            float* __restrict__ oH, float* __restrict__ oU, float* __restrict__ oV,
+            float dx, float dy, DtSrc dts, float g, BCs bc, RedPtrs red) {
+    using namespace tma;
+    using G = Geo<CPL>;
+    // CPL = 4 keeps every TMA box start (tensor column 120 j) 16-byte aligned;
+    // narrower lanes would need wider ghost margins to stay aligned.
+    static_assert(CPL == 4, "the strip geometry assumes 4 cells (one float4) per lane");
+    constexpr int DM = FAST ? DIV_FAST : DIV_GUARD;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * WARPS + warp;
+    const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
+    const int tx = xs + 3;                               // its tensor column
+    if (xs + CPL > nx) return;                           // strip owns nothing (ragged last band)
+    const int y0 = 1 + blockIdx.y * seg;                 // first interior row of the segment
+    const int nrows = min(seg, ny - y0 + 1);
+    const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
+    const int nstages = (nload + R - 1) / R;
+    const uint32_t ring = sbase + warp * G::WARP_RING;
+    const uint32_t full = sbase + WARPS * G::WARP_RING + warp * S * 8;
+
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < S - 1 && k < nstages; ++k)
+            issue_stage<CPL>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, y0 - 1 + k * R);
+    }
+    __syncwarp();
+
+    const float dt = resolve_dt<float>(dts);
+    const Coef<float> c = make_coef<float>(dx, dy, dt, g);
+    const float dmin = dx < dy ? dx : dy;
+    const int X = xs + CPL * lane;             // full column of cell 0 of this lane
+    const bool owner = (lane >= 1) && (lane <= 30) && (X <= nx);   // nx % CPL == 0
+    // cells whose loaded data is not part of the grid (padding left of column
+    // 0 in strip 0, zero-fill right of column nx+1) are replaced by a lake at
+    // rest so they cannot trip the exact-division guard; they feed no owned cell
+    int bad = 0;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i)
+        if (X + i < 0 || X + i > nx + 1) bad |= 1 << i;
+    const bool any_bad = __any_sync(0xffffffffu, bad != 0);
+    const bool edge_rows = (y0 == 1) || (y0 + nrows - 1 == ny);
+    const bool edge_cols = owner && ((X == 1) || (X + CPL - 1 == nx));
+    const uint32_t lane_off = 4u * CPL * lane;
+
+    CellQ<float> pc[CPL];              // previous row's cells
+    FaceF<float> pxl, pxr[CPL];        // previous row's x-face fluxes
+    FaceF<float> ydn[CPL];             // y-face below the previous row
+    RedAcc<float> acc;
+    acc.init();
+    bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
+    int fix_rows = 0;
+    constexpr int UNR = FAST ? R : FKC_EXACT_UNROLL;  // exact: keep the loop body inside the I-cache
+
+    for (int k = 0; k < nstages; ++k) {
+        const int s = k % S;
+        // refill the slot freed by stage k-1 (every lane finished reading it)
+        if (lane == 0 && k + S - 1 < nstages) {
+            const int kn = k + S - 1;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_stage<CPL>(ring + (kn % S) * G::STAGE_BYTES, full + 8 * (kn % S), &tmH, &tmU, &tmV, tx,
+                             y0 - 1 + kn * R);
+        }
+        mbar_wait(full + 8 * s, (k / S) & 1, red.err);
+        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off;
+#pragma unroll UNR
+        for (int r = 0; r < R; ++r) {
+            const int n = k * R + r;              // loaded row index; row y0-1+n
+            VecF<CPL> hv = lds_vec<CPL>(st + r * (G::LOAD * 4));
+            VecF<CPL> uv = lds_vec<CPL>(st + G::FIELD_BYTES + r * (G::LOAD * 4));
+            VecF<CPL> vv = lds_vec<CPL>(st + 2 * G::FIELD_BYTES + r * (G::LOAD * 4));
+            if (any_bad) {
+#pragma unroll
+                for (int i = 0; i < CPL; ++i)
+                    if (bad & (1 << i)) { hv.v[i] = 1.f; uv.v[i] = 0.f; vv.v[i] = 0.f; }
+            }
+            const bool have_prev = n >= 1;
+            const bool want_x = (n >= 1) && (n <= nrows);
+            CellQ<float> nc[CPL];
+            FaceF<float> yup[CPL], nxl, nxr[CPL];
+            bool ok = true;
+            if (FAST) {
+                row_faces<DIV_FAST, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+            } else {
+                // exact mode, warp-uniform per row: lean guarded division;
+                // if any lane saw a non-benign operand, redo the row with the
+                // never-failing DIV_FIXUP variant (scaled tiny numerators,
+                // per-numerator __fdiv_rn for the rest).  Tiny-valued regions
+                // are contiguous along the sweep, so after a row needed the
+                // fixup variant the next rows start with it and the lean
+                // variant is retried every 16 rows.
+                if (!fix_mode && !FKC_EXACT_ALWAYS_FIXUP) {
+                    row_faces<DIV_GUARD, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    if (__any_sync(0xffffffffu, !ok)) {
+                        fix_mode = true;
+                        fix_rows = 0;
+                        row_faces<DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    }
+                } else {
+                    row_faces<DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    if (++fix_rows >= 16) fix_mode = false;
+                }
+            }
+            // full-step update of the previous row (row y0 + n - 2)
+            if (n >= 2 && n <= nrows + 1) {
+                const int y = y0 + n - 2;
+                float oh[CPL], ou[CPL], ov[CPL];
+#pragma unroll
+                for (int i = 0; i < CPL; ++i)
+                    update_cell<float, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i],
+                                           ydn[i], yup[i], c, oh[i], ou[i], ov[i]);
+                if (owner) {
+                    const int64_t off = (int64_t)y * pitch + X;
+                    stg_vec<CPL>(oH + off, oh);
+                    stg_vec<CPL>(oU + off, ou);
+                    stg_vec<CPL>(oV + off, ov);
+                    // fused boundary fill of the output halo
+                    if (edge_rows && (y == 1 || y == ny)) {
+                        const bool refl = (y == 1 && bc.s[SIDE_D] == BC_REFL) || (y == ny && bc.s[SIDE_U] == BC_REFL);
+                        const bool per = (y == 1 && bc.s[SIDE_U] == BC_PER) || (y == ny && bc.s[SIDE_D] == BC_PER);
+                        if (refl) {
+                            const int64_t o2 = (int64_t)(y == 1 ? 0 : ny + 1) * pitch + X;
+                            stg_vec<CPL>(oH + o2, oh);
+                            stg_vec<CPL>(oU + o2, ou);
+                            stg_vec<CPL>(oV + o2, ov, -1.0f);
+                        }
+                        if (per) {
+                            const int64_t o2 = (int64_t)(y == 1 ? ny + 1 : 0) * pitch + X;
+                            stg_vec<CPL>(oH + o2, oh);
+                            stg_vec<CPL>(oU + o2, ou);
+                            stg_vec<CPL>(oV + o2, ov);
+                        }
+                    }
+                    if (edge_cols) {
+                        if (X == 1)
+                            emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, 1, y, oh[0], ou[0], ov[0], false);
+                        if (X + CPL - 1 == nx)
+                            emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, nx, y, oh[CPL - 1], ou[CPL - 1],
+                                              ov[CPL - 1], false);
+                    }
+                    if (RED) {
+                        double m = 0.0;
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) m += (double)oh[i];
+                        acc.mass += m;
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i)
+                            acc.add_cell(oh[i], ou[i], ov[i], g, dmin, red.cfl_min != nullptr, red.err != nullptr);
+                    }
+                }
+            }
+            // shift the register window (renamed away by the unrolled loop)
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) { pc[i] = nc[i]; ydn[i] = yup[i]; pxr[i] = nxr[i]; }
+            pxl = nxl;
+        }
+        __syncwarp();
+    }
+    if (RED) warp_reduce_commit<float>(acc, red, lane);
+}
+
+}  // namespace fkc
