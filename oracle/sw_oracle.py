@@ -217,6 +217,35 @@ def apply_boundary(H, U, V, mode: str = "reflective"):
     return H, U, V
 
 
+def apply_boundary_sides(H, U, V, sides):
+    """apply_boundary with a per-side spec (left, right, down, up), each
+    'reflective' | 'periodic' | 'none' ('none' = filled by a halo exchange
+    in a decomposed run).  Same order as apply_boundary: columns over the
+    interior rows, then rows over all columns."""
+    left, right, down, up = sides
+    if left == "reflective":
+        H[1:-1, 0] = H[1:-1, 1]; U[1:-1, 0] = -U[1:-1, 1]; V[1:-1, 0] = V[1:-1, 1]
+    elif left == "periodic":
+        for A in (H, U, V):
+            A[1:-1, 0] = A[1:-1, -2]
+    if right == "reflective":
+        H[1:-1, -1] = H[1:-1, -2]; U[1:-1, -1] = -U[1:-1, -2]; V[1:-1, -1] = V[1:-1, -2]
+    elif right == "periodic":
+        for A in (H, U, V):
+            A[1:-1, -1] = A[1:-1, 1]
+    if down == "reflective":
+        H[0, :] = H[1, :]; U[0, :] = U[1, :]; V[0, :] = -V[1, :]
+    elif down == "periodic":
+        for A in (H, U, V):
+            A[0, :] = A[-2, :]
+    if up == "reflective":
+        H[-1, :] = H[-2, :]; U[-1, :] = U[-2, :]; V[-1, :] = -V[-2, :]
+    elif up == "periodic":
+        for A in (H, U, V):
+            A[-1, :] = A[1, :]
+    return H, U, V
+
+
 def cfl_bound(H, U, V, dx, dy, g: float = 9.8):
     """Per-cell CFL bound min(dx,dy)/(sqrt(g h) + max(|hu|,|hv|)/h)
     (SPEC.md:508-516), field precision, this exact op order."""

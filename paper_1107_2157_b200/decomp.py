@@ -1,0 +1,423 @@
+"""2-D domain decomposition of the shallow-water grid over GPUs (one process
+per GPU) with a one-cell halo exchange per step -- SURVEY.md 8(e).
+
+The reference runs on one device (the paper leaves MPI generation as future
+work).  Every cell update needs only the 1-cell ring of
+H, U, V (a 3x3 cross stencil; corners are never read), so a Cartesian split
+needs exactly one exchange of boundary lines per step:
+
+* rank (rx, ry) of a px x py grid owns a rectangle of the global interior;
+* the step kernel applies the physical boundary condition on the sides that
+  touch the global boundary and leaves the other halo sides alone
+  (``FKC_BC_NONE``);
+* after the step, each rank sends the outermost interior row/column of the
+  new H, U, V to the neighbour on that side, which writes it into its halo
+  (periodic boundaries wrap around the process grid; an axis with one rank
+  wraps locally in the kernel).
+
+Per-cell arithmetic is unchanged by the decomposition, so the decomposed
+state is bit-identical to the single-domain state (tested).  Transports:
+``DistTransport`` (torch.distributed P2P: NCCL on GPUs, gloo in the CPU
+tests) and ``LocalTransport`` (several sub-domains in one process, used to
+validate the GPU path on a single device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .region import Extent
+
+LEFT, RIGHT, DOWN, UP = 0, 1, 2, 3
+OPPOSITE = {LEFT: RIGHT, RIGHT: LEFT, DOWN: UP, UP: DOWN}
+# transfer order: every rank issues the same sequence, so P2P messages
+# between any pair of ranks match in order (NCCL) and by tag (gloo)
+EXCHANGE_ORDER = (RIGHT, LEFT, UP, DOWN)
+
+
+def choose_grid(n: int) -> Tuple[int, int]:
+    """px x py with py >= px (more of the halo in contiguous rows)."""
+    best = (1, n)
+    for px in range(1, int(n ** 0.5) + 1):
+        if n % px == 0:
+            best = (px, n // px)
+    return best
+
+
+@dataclass(frozen=True)
+class Tile:
+    rank: int
+    rx: int
+    ry: int
+    x0: int       # global interior column offset (0-based) of the first owned column
+    y0: int
+    nx: int
+    ny: int
+
+
+class CartGrid:
+    """px x py Cartesian split of an NX x NY interior; rank = ry*px + rx."""
+
+    def __init__(self, px: int, py: int, NX: int, NY: int, boundary: str = "reflective"):
+        if px < 1 or py < 1 or NX < px or NY < py:
+            raise ValueError("bad process grid")
+        self.px, self.py, self.NX, self.NY = px, py, NX, NY
+        self.boundary = boundary
+        self.periodic = boundary == "periodic"
+
+    @property
+    def size(self) -> int:
+        return self.px * self.py
+
+    @staticmethod
+    def _split(n: int, parts: int, i: int) -> Tuple[int, int]:
+        base, extra = divmod(n, parts)
+        start = i * base + min(i, extra)
+        return start, base + (1 if i < extra else 0)
+
+    def tile(self, rank: int) -> Tile:
+        rx, ry = rank % self.px, rank // self.px
+        x0, nx = self._split(self.NX, self.px, rx)
+        y0, ny = self._split(self.NY, self.py, ry)
+        return Tile(rank, rx, ry, x0, y0, nx, ny)
+
+    def neighbor(self, rank: int, side: int) -> Optional[int]:
+        """Rank across `side`, None at a physical (non-periodic) boundary or
+        when the axis has a single rank (the kernel wraps locally)."""
+        t = self.tile(rank)
+        rx, ry = t.rx, t.ry
+        if side in (LEFT, RIGHT):
+            if self.px == 1:
+                return None
+            rx += -1 if side == LEFT else 1
+            if not 0 <= rx < self.px:
+                if not self.periodic:
+                    return None
+                rx %= self.px
+        else:
+            if self.py == 1:
+                return None
+            ry += -1 if side == DOWN else 1
+            if not 0 <= ry < self.py:
+                if not self.periodic:
+                    return None
+                ry %= self.py
+        return ry * self.px + rx
+
+    def local_bc(self, rank: int) -> Tuple[str, str, str, str]:
+        """Per-side boundary handling for the step kernel of `rank`."""
+        out = []
+        for side in (LEFT, RIGHT, DOWN, UP):
+            single = self.px == 1 if side in (LEFT, RIGHT) else self.py == 1
+            if self.neighbor(rank, side) is not None:
+                out.append("none")                  # filled by the exchange
+            elif self.periodic and single:
+                out.append("periodic")              # local wrap
+            else:
+                out.append(self.boundary)           # physical wall
+        return tuple(out)
+
+
+# ---------------------------------------------------------------------------
+# line pack / unpack
+# ---------------------------------------------------------------------------
+
+def _line_len(side: int, nx: int, ny: int) -> int:
+    return ny if side in (LEFT, RIGHT) else nx
+
+
+class NativeLines:
+    """Pack / unpack boundary lines with the C-ABI kernels (device fields)."""
+
+    def __init__(self, stream=None):
+        self.stream = stream
+
+    def _sp(self):
+        import torch
+        s = self.stream if self.stream is not None else torch.cuda.current_stream()
+        return s.cuda_stream
+
+    def pack(self, st, side: int, buf):
+        from .swdemo import _grid
+        g = _grid(st.H)
+        N.check(N.lib().fkc_halo_pack(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, side, buf.data_ptr(),
+                                      self._sp()))
+
+    def unpack(self, st, side: int, buf):
+        from .swdemo import _grid
+        g = _grid(st.H)
+        N.check(N.lib().fkc_halo_unpack(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, side, buf.data_ptr(),
+                                        self._sp()))
+
+
+class TorchLines:
+    """Pack / unpack with tensor slicing -- for CPU states in the gloo tests
+    (state fields are (ny+2, nx+2) torch tensors or objects with ``.data``)."""
+
+    @staticmethod
+    def _arrays(st):
+        return [getattr(f, "data", f) for f in (st.H, st.U, st.V)]
+
+    def pack(self, st, side: int, buf):
+        arrs = self._arrays(st)
+        for k, a in enumerate(arrs):
+            line = {LEFT: a[1:-1, 1], RIGHT: a[1:-1, -2], DOWN: a[1, 1:-1], UP: a[-2, 1:-1]}[side]
+            n = line.shape[0]
+            buf[k * n:(k + 1) * n].copy_(line)
+
+    def unpack(self, st, side: int, buf):
+        arrs = self._arrays(st)
+        for k, a in enumerate(arrs):
+            line = {LEFT: a[1:-1, 0], RIGHT: a[1:-1, -1], DOWN: a[0, 1:-1], UP: a[-1, 1:-1]}[side]
+            n = line.shape[0]
+            line.copy_(buf[k * n:(k + 1) * n])
+
+
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+class DistTransport:
+    """Neighbour P2P over torch.distributed (NCCL across GPUs, gloo on CPU).
+    All ops of one exchange go into one batch_isend_irecv group."""
+
+    TAG = {RIGHT: 11, LEFT: 12, UP: 13, DOWN: 14}
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, sends: Dict[int, Tuple[int, object]], recvs: Dict[int, Tuple[int, object]]):
+        """sends/recvs: side -> (peer rank, buffer).  A line sent towards
+        `side` lands in the peer's halo on OPPOSITE[side]."""
+        dist = self.dist
+        ops = []
+        for side in EXCHANGE_ORDER:
+            if side in sends:
+                peer, buf = sends[side]
+                ops.append(dist.P2POp(dist.isend, buf, peer, self.group, self.TAG[side]))
+            opp = OPPOSITE[side]
+            if opp in recvs:      # the message travelling towards `side` arrives on our OPPOSITE side
+                peer, buf = recvs[opp]
+                ops.append(dist.P2POp(dist.irecv, buf, peer, self.group, self.TAG[side]))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+class HaloExchanger:
+    """Send the outermost interior lines of a state to the neighbours and
+    fill its halo lines from theirs."""
+
+    def __init__(self, grid: CartGrid, rank: int, transport, lines, device=None, dtype=None):
+        import torch
+        self.grid, self.rank, self.transport, self.lines = grid, rank, transport, lines
+        t = grid.tile(rank)
+        self.nbr = {s: grid.neighbor(rank, s) for s in (LEFT, RIGHT, DOWN, UP)}
+        dtype = dtype or torch.float32
+        self.send = {s: torch.empty(3 * _line_len(s, t.nx, t.ny), dtype=dtype, device=device)
+                     for s, p in self.nbr.items() if p is not None}
+        self.recv = {s: torch.empty_like(b) for s, b in self.send.items()}
+
+    def exchange(self, st):
+        for s in self.send:
+            self.lines.pack(st, s, self.send[s])
+        self.transport.exchange({s: (self.nbr[s], b) for s, b in self.send.items()},
+                                {s: (self.nbr[s], b) for s, b in self.recv.items()})
+        for s in self.recv:
+            self.lines.unpack(st, s, self.recv[s])
+
+
+class LocalTransport:
+    """All sub-domains in one process: exchange = buffer copies."""
+
+    def __init__(self, grid: CartGrid):
+        self.grid = grid
+
+    def exchange_all(self, exchangers: List[HaloExchanger], states):
+        for ex, st in zip(exchangers, states):
+            for s in ex.send:
+                ex.lines.pack(st, s, ex.send[s])
+        for ex in exchangers:
+            for s, buf in ex.recv.items():
+                src = exchangers[ex.nbr[s]]
+                buf.copy_(src.send[OPPOSITE[s]])
+        for ex, st in zip(exchangers, states):
+            for s in ex.recv:
+                ex.lines.unpack(st, s, ex.recv[s])
+
+
+# ---------------------------------------------------------------------------
+# initial state of a tile (same f64 formula as swdemo.init_state)
+# ---------------------------------------------------------------------------
+
+def gaussian_tile(grid: CartGrid, rank: int, precision="f32", dx=1.0, dy=1.0, base=1.0, amplitude=0.4,
+                  center=None, width=None) -> np.ndarray:
+    """Interior (ny, nx) of the global Gaussian hump restricted to the tile,
+    evaluated exactly as swdemo.init_state / oracle.init_state do."""
+    t = grid.tile(rank)
+    NX, NY = grid.NX, grid.NY
+    cx, cy = center if center is not None else (NX * dx / 2.0, NY * dy / 2.0)
+    w = width if width is not None else NX * dx / 8.0
+    xc = (np.arange(t.x0, t.x0 + t.nx, dtype=np.float64) + 0.5) * dx - cx
+    yc = (np.arange(t.y0, t.y0 + t.ny, dtype=np.float64) + 0.5) * dy - cy
+    h = base + amplitude * np.exp(-(xc[None, :] ** 2 + yc[:, None] ** 2) / (w * w))
+    return h.astype({"f32": np.float32, "f64": np.float64}[precision])
+
+
+# ---------------------------------------------------------------------------
+# distributed simulation (one process per GPU)
+# ---------------------------------------------------------------------------
+
+class DistributedSimulation:
+    """One rank's tile of a decomposed run: step kernel with per-side BC,
+    then halo exchange of the new state, double-buffer swap.
+
+    ``dt`` is fixed (``cfg.dt``) -- the weak-scaling benchmark; for CFL-driven
+    runs the per-rank bound from the fused reduction is all-reduced (MIN).
+    """
+
+    def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None):
+        import torch
+        from . import swdemo
+        from .field import DeviceField, Field
+        self.cfg, self.grid, self.rank = cfg, grid, rank
+        self.tile = grid.tile(rank)
+        self.bc = grid.local_bc(rank)
+        self.stream = stream
+        t = self.tile
+        full = Extent(t.nx + 2, t.ny + 2)
+        h = gaussian_tile(grid, rank, cfg.precision, cfg.dx, cfg.dy, cfg.base, cfg.amplitude, cfg.center,
+                          cfg.width)
+        H = Field.zeros(full, cfg.precision)
+        H.data[1:-1, 1:-1] = h
+        st = swdemo.SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
+                            cfg.g, cfg.dx, cfg.dy).to_device(device)
+        self.a = st
+        self.b = swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx, st.dy)
+        tdt = torch.float32 if cfg.precision == "f32" else torch.float64
+        self.ex = HaloExchanger(grid, rank, DistTransport(group), NativeLines(stream), st.H.storage.device, tdt)
+        swdemo.apply_boundary(self.a, self.bc, stream)
+        self.ex.exchange(self.a)
+        self.n = 0
+
+    def advance(self, steps: int):
+        from . import swdemo
+        for _ in range(steps):
+            src, dst = (self.a, self.b) if self.n % 2 == 0 else (self.b, self.a)
+            swdemo.advance(src, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant, out=dst,
+                           stream=self.stream)
+            self.ex.exchange(dst)
+            self.n += 1
+        return self
+
+    def state(self):
+        return self.a if self.n % 2 == 0 else self.b
+
+
+def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None):
+    """All px*py tiles in one process on one device (LocalTransport): the
+    GPU-side validation of the decomposed path.  Returns the tiles' states."""
+    from . import swdemo
+    from .field import Field
+    grid = CartGrid(px, py, cfg.nx, cfg.ny, cfg.boundary)
+    states, others, exs = [], [], []
+    for r in range(grid.size):
+        t = grid.tile(r)
+        full = Extent(t.nx + 2, t.ny + 2)
+        H = Field.zeros(full, cfg.precision)
+        H.data[1:-1, 1:-1] = gaussian_tile(grid, r, cfg.precision, cfg.dx, cfg.dy, cfg.base, cfg.amplitude,
+                                           cfg.center, cfg.width)
+        st = swdemo.SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
+                            cfg.g, cfg.dx, cfg.dy).to_device(device)
+        swdemo.apply_boundary(st, grid.local_bc(r))
+        states.append(st)
+        others.append(swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx,
+                                     st.dy))
+        import torch
+        exs.append(HaloExchanger(grid, r, None, NativeLines(), st.H.storage.device,
+                                 torch.float32 if cfg.precision == "f32" else torch.float64))
+    lt = LocalTransport(grid)
+    lt.exchange_all(exs, states)
+    for _ in range(steps):
+        for r in range(grid.size):
+            swdemo.advance(states[r], cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant, out=others[r])
+        states, others = others, states
+        lt.exchange_all(exs, states)
+    return grid, states
+
+
+def gather_interior(grid: CartGrid, tiles: Sequence[np.ndarray]) -> np.ndarray:
+    """Assemble per-rank interiors (ny, nx) into the global interior."""
+    out = np.empty((grid.NY, grid.NX), dtype=tiles[0].dtype)
+    for r, a in enumerate(tiles):
+        t = grid.tile(r)
+        out[t.y0:t.y0 + t.ny, t.x0:t.x0 + t.nx] = a
+    return out
+
+
+# ---------------------------------------------------------------------------
+# bench entry (torchrun, N > 1): weak scaling, 16384^2 cells per GPU
+# ---------------------------------------------------------------------------
+
+def bench_main(args, rank: int, world: int) -> int:
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import swdemo
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    px, py = choose_grid(world)
+    n = args.n
+    grid = CartGrid(px, py, px * n, py * n, "reflective")
+    # fixed dt = 0.3 * stable_dt of the initial global state (h max 1.4, u = v = 0)
+    dt = 0.3 * 1.0 / float(np.sqrt(np.float32(9.8) * np.float32(1.4)))
+    cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream)
+        sim.advance(args.warmup)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        sim.advance(args.steps)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    cells = grid.NX * grid.NY
+    value = cells * args.steps / (total_ms / 1e3) / 1e9
+    if rank == 0:
+        from bench import BYTES_PER_CELL, peaks
+        peak, src = peaks()
+        per_gpu_gbs = BYTES_PER_CELL["f32"] * (cells / world) * args.steps / (total_ms / 1e3) / 1e9
+        line = {"metric": "Gcell-updates/s (shallow-water step)", "value": round(value, 3),
+                "unit": "Gcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
+                "config": {"workload": f"shallow-water {n}x{n} fp32 per GPU, 2-D decomposed {px}x{py}, "
+                                       "one-cell halo exchange per step (NCCL P2P)",
+                           "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
+                "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
+                             "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
+                             "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
+                "gpu_launches": args.steps * (1 + 2 * len(sim.ex.send))}
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
