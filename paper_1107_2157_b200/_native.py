@@ -25,7 +25,7 @@ ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
 
 EXPORTS = (
     "fkc_sw_step", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
-    "fkc_region_cpy", "fkc_cshift", "fkc_halo_pack", "fkc_halo_unpack",
+    "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
     "fkc_set_tma_segment", "fkc_test_div_f32", "fkc_last_error", "fkc_abi_version",
 )
 
@@ -93,6 +93,7 @@ def lib():
         "fkc_sw_reduce_reset": [ctypes.POINTER(Reduce), vp],
         "fkc_region_cpy": [i32, vp, i32, i32, i64, ctypes.POINTER(i32), vp, i64, vp],
         "fkc_cshift": [i32, vp, i32, i32, i64, i32, i64, vp, i64, vp],
+        "fkc_copy2d": [vp, i64, vp, i64, i64, i64, vp],
         "fkc_halo_pack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
         "fkc_halo_unpack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
         "fkc_set_tma_segment": [ctypes.c_int],

@@ -277,6 +277,18 @@ int fkc_sw_apply_boundary(const fkc_grid* g, void* H, void* U, void* V, const in
     return check_launch("sw_bc_kernel");
 }
 
+int fkc_copy2d(void* dst, int64_t dst_pitch_bytes, const void* src, int64_t src_pitch_bytes,
+               int64_t width_bytes, int64_t height, void* stream) {
+    if (!dst || !src || width_bytes < 0 || height < 0 || dst_pitch_bytes < width_bytes ||
+        src_pitch_bytes < width_bytes)
+        return fail(FKC_EUSAGE, "bad 2-D copy arguments");
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dst_pitch_bytes, src, (size_t)src_pitch_bytes,
+                                      (size_t)width_bytes, (size_t)height, cudaMemcpyDefault,
+                                      (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+    return FKC_OK;
+}
+
 int fkc_sw_reduce_reset(const fkc_sw_reduce* red, void* stream) {
     if (!red) return fail(FKC_EUSAGE, "null reduce");
     reduce_reset_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(to_red(*red));

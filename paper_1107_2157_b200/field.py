@@ -141,16 +141,52 @@ class DeviceField:
         d.copy_from_host(f.data, non_blocking=non_blocking)
         return d
 
-    def copy_from_host(self, arr, non_blocking: bool = False):
+    def _stream(self, stream=None) -> int:
         torch = _torch()
-        src = arr if isinstance(arr, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(arr))
-        self.data.copy_(src, non_blocking=non_blocking)
+        s = stream if stream is not None else torch.cuda.current_stream(self.storage.device)
+        return s.cuda_stream
+
+    def copy_from_host(self, arr, non_blocking: bool = False, stream=None):
+        """Host (ny, nx) array -> device, one pitched DMA (fkc_copy2d).
+        Pinned host memory gives full PCIe bandwidth and, with
+        non_blocking=True, an asynchronous copy on `stream`."""
+        from . import _native as N
+        torch = _torch()
+        a = arr.numpy() if isinstance(arr, torch.Tensor) else np.asarray(arr)
+        if a.shape != (self.full.ny, self.full.nx) or a.dtype != dtype_of(self.precision):
+            raise ValueError(f"host array {a.shape}/{a.dtype} does not match {self!r}")
+        if a.strides[1] != a.itemsize:
+            a = np.ascontiguousarray(a)
+        it = a.itemsize
+        sp = self._stream(stream)
+        N.check(N.lib().fkc_copy2d(self.ptr, self.pitch * it, a.ctypes.data, a.strides[0],
+                                   self.full.nx * it, self.full.ny, sp))
+        if not non_blocking:
+            torch.cuda.current_stream(self.storage.device).synchronize() if stream is None else stream.synchronize()
         return self
 
-    def to_numpy(self) -> np.ndarray:
-        return self.data.cpu().numpy()
+    def copy_to_host(self, out: np.ndarray, non_blocking: bool = False, stream=None) -> np.ndarray:
+        """Device -> host (ny, nx) array (pinned for full bandwidth)."""
+        from . import _native as N
+        torch = _torch()
+        if out.shape != (self.full.ny, self.full.nx) or out.dtype != dtype_of(self.precision) \
+                or out.strides[1] != out.itemsize:
+            raise ValueError("output array does not match the field")
+        it = out.itemsize
+        N.check(N.lib().fkc_copy2d(out.ctypes.data, out.strides[0], self.ptr, self.pitch * it,
+                                   self.full.nx * it, self.full.ny, self._stream(stream)))
+        if not non_blocking:
+            torch.cuda.current_stream(self.storage.device).synchronize() if stream is None else stream.synchronize()
+        return out
 
-    def to_field(self) -> Field:
+    def to_numpy(self) -> np.ndarray:
+        out = np.empty((self.full.ny, self.full.nx), dtype_of(self.precision))
+        return self.copy_to_host(out)
+
+    def to_field(self, out: Field | None = None) -> Field:
+        if out is not None:
+            self.copy_to_host(out.data)
+            return out
         return Field(self.full, self.to_numpy(), self.precision)
 
     def empty_like(self) -> "DeviceField":

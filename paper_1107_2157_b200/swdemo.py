@@ -123,9 +123,15 @@ class SWState:
         return SWState(*(DeviceField.from_field(f, device) for f in (self.H, self.U, self.V)),
                        self.g, self.dx, self.dy, self.t)
 
-    def to_host(self) -> "SWState":
+    def to_host(self, out: Optional["SWState"] = None) -> "SWState":
+        """Device -> host Fields (into `out`'s arrays when given, e.g. pinned)."""
         if not self.on_device:
             return self
+        if out is not None:
+            for name in ("H", "U", "V"):
+                getattr(self, name).to_field(getattr(out, name))
+            out.g, out.dx, out.dy, out.t = self.g, self.dx, self.dy, self.t
+            return out
         return SWState(self.H.to_field(), self.U.to_field(), self.V.to_field(),
                        self.g, self.dx, self.dy, self.t)
 
@@ -358,7 +364,7 @@ class Simulation:
     def _args_for(self, i: int) -> N.StepArgs:
         src, dst = (self.a, self.b) if i % 2 == 0 else (self.b, self.a)
         cfg = self.cfg
-        red = self.slots.reduce_struct(i + 1) if self.diag else None
+        red = self.slots.reduce_struct(i + 1, cfl=cfg.dt is None) if self.diag else None
         bound = self.slots.addr(i, 3) if cfg.dt is None else None
         return _step_args(src, dst, cfg.dt if cfg.dt is not None else 0.0, self.boundary, cfg.mode,
                           cfg.variant, red, bound, cfg.cfl_factor)
@@ -407,14 +413,14 @@ class Simulation:
 
 
 def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
-        to_host: bool = False) -> RunResult:
+        to_host: bool = False, out: Optional[SWState] = None) -> RunResult:
     """Time loop: apply_boundary -> dt -> advance -> swap ->
     diagnostics (mass, max|hu|, max|hv|, dt), aborting on non-finite values.
 
     The whole loop is enqueued on the GPU; per-step diagnostics come from the
     reductions fused into each step and are read back once at the end.
     A host ``state`` is uploaded first; ``to_host=True`` returns the final
-    state as host Fields.
+    state as host Fields (written into ``out``'s arrays when given).
     """
     if engine not in ENGINES:
         raise ValueError(f"engine {engine!r} is not provided by the B200 package "
@@ -422,6 +428,6 @@ def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
     sim = Simulation(cfg, state=state, diagnostics=True)
     sim.advance(cfg.steps)
     res = sim.rows()
-    if to_host:
-        res.state = res.state.to_host()
+    if to_host or out is not None:
+        res.state = res.state.to_host(out)
     return res
