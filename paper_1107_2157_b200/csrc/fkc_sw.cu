@@ -169,10 +169,10 @@ int g_seg_override = 0;
 
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
-    // >= ~4 waves of resident CTAs, while keeping the 2 halo rows per
+    // >= ~32 waves of resident CTAs (small tail; measured best at 16384^2), keeping the 2 halo rows per
     // segment a small fraction of the sweep
     int seg = 256;
-    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < (int64_t)148 * ctas_per_sm * 4) seg /= 2;
+    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < (int64_t)148 * ctas_per_sm * 32) seg /= 2;
     return seg;
 }
 
@@ -188,7 +188,7 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const fkc_grid& g = a->grid;
     const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
     const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
-    const int seg = pick_seg(nbands, g.ny, G::CTAS_PER_SM);
+    const int seg = pick_seg(nbands, g.ny, G::template ctas_per_sm<FAST>());
     dim3 grd(nbands, (g.ny + seg - 1) / seg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
     kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,

@@ -24,8 +24,20 @@
 namespace fkc {
 namespace tma {
 constexpr int WARPS = 4;                 // warps (strips) per CTA
-constexpr int R = 4;                     // rows per stage
-constexpr int S = 4;                     // ring stages per warp
+#ifndef FKC_TMA_R
+#define FKC_TMA_R 4
+#endif
+#ifndef FKC_TMA_S
+#define FKC_TMA_S 3
+#endif
+#ifndef FKC_TMA_CTAS_FAST
+#define FKC_TMA_CTAS_FAST 3   // fast kernel: <= 168 registers -> 12 warps per SM
+#endif
+#ifndef FKC_TMA_CTAS_EXACT
+#define FKC_TMA_CTAS_EXACT 2  // exact kernel: ~190 registers -> 8 warps per SM
+#endif
+constexpr int R = FKC_TMA_R;             // rows per stage
+constexpr int S = FKC_TMA_S;             // ring stages per warp
 template <int CPL> struct Geo {
     static constexpr int LOAD = 32 * CPL;                 // columns loaded per strip
     static constexpr int OWN = 30 * CPL;                  // columns owned per strip
@@ -33,7 +45,7 @@ template <int CPL> struct Geo {
     static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
     static constexpr int WARP_RING = S * STAGE_BYTES;
     static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
-    static constexpr int CTAS_PER_SM = CPL == 4 ? 2 : 4;   // register budget: 255 / 128 regs
+    template <bool FAST> static constexpr int ctas_per_sm() { return FAST ? FKC_TMA_CTAS_FAST : FKC_TMA_CTAS_EXACT; }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
 constexpr int THREADS = WARPS * 32;
@@ -156,7 +168,7 @@ __device__ __forceinline__ void row_faces(const VecF<CPL>& h, const VecF<CPL>& u
 // owns columns [1 + OWN j, OWN (j+1)] and loads full columns
 // [1 + OWN j - CPL, OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
 template <int CPL, bool FAST, bool RED>
-__global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::CTAS_PER_SM)
+__global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::template ctas_per_sm<FAST>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg,
             float* __restrict__ oH, float* __restrict__ oU, float* __restrict__ oV,
