@@ -169,10 +169,14 @@ int g_seg_override = 0;
 
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
-    // >= ~32 waves of resident CTAs (small tail; measured best at 16384^2), keeping the 2 halo rows per
-    // segment a small fraction of the sweep
-    int seg = 256;
-    while (seg > 32 && (int64_t)nbands * ((ny + seg - 1) / seg) < (int64_t)148 * ctas_per_sm * 32) seg /= 2;
+    // Rows per CTA segment.  Short segments shrink the tail of the last wave
+    // of CTAs; long ones amortise the 2 halo rows and the pipeline prologue.
+    // Measured on B200 (profiles/r01/seg_sweep.json, fast mode, 1024^2 ..
+    // 16384^2): the best length tracks ny/256, clamped to [8, 32].
+    (void)nbands;
+    (void)ctas_per_sm;
+    int seg = 8;
+    while (seg < 32 && seg * 2 <= ny / 256) seg *= 2;
     return seg;
 }
 

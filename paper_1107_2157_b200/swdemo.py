@@ -380,6 +380,32 @@ class Simulation:
             self.n += 1
         return self
 
+    def capture(self, steps: int):
+        """CUDA-graph the next `steps` steps (fixed dt, no diagnostics) for
+        launch-bound small grids: returns a callable that replays them.
+        `steps` must be even so the double buffers end where they started;
+        each replay advances the state by `steps` steps."""
+        torch = self.torch
+        if steps % 2 or self.diag:
+            raise ValueError("capture needs an even step count and diagnostics off")
+        stream = self.stream if self.stream is not None else torch.cuda.Stream()
+        self.advance(2)                      # warm-up outside capture (tensor maps, attributes)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = self.n
+        with torch.cuda.graph(graph, stream=stream):
+            L = N.lib()
+            sp = stream.cuda_stream
+            for k in range(steps):
+                a = self._args_for(n0 + k)
+                N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+
+        def replay():
+            graph.replay()
+            self.n += steps
+        replay.graph = graph
+        return replay
+
     def state(self) -> SWState:
         s = self.a if self.n % 2 == 0 else self.b
         return s
