@@ -172,6 +172,9 @@ def main():
                          "exact: bit-identical to the oracle")
     ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
     ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 halo exchange: peer = fused into the step kernel over NVLink peer memory "
+                         "(CUDA IPC + mailbox flags); nccl = pack + NCCL send/recv + unpack (baseline)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the other-mode timing (profiling runs)")

@@ -26,8 +26,10 @@ ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
 EXPORTS = (
     "fkc_sw_step", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
+    "fkc_ipc_export", "fkc_ipc_open", "fkc_ipc_close",
     "fkc_set_tma_segment", "fkc_test_div_f32", "fkc_last_error", "fkc_abi_version",
 )
+ABI_VERSION = 2
 
 
 class NativeUnavailable(RuntimeError):
@@ -51,6 +53,17 @@ class Reduce(ctypes.Structure):
                 ("err", ctypes.c_void_p)]
 
 
+class PeerLine(ctypes.Structure):
+    """fkc_peer_line: neighbour address of our cell (0,0) image per field + stride."""
+    _fields_ = [("p", ctypes.c_void_p * 3), ("stride", ctypes.c_int64)]
+
+
+class Sync(ctypes.Structure):
+    """fkc_sync: per-side mailbox words, edge-writer counters, epoch."""
+    _fields_ = [("wait", ctypes.c_void_p * 4), ("signal", ctypes.c_void_p * 4),
+                ("counter", ctypes.c_void_p), ("epoch", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+
+
 class StepArgs(ctypes.Structure):
     _fields_ = [("grid", Grid),
                 ("H", ctypes.c_void_p), ("U", ctypes.c_void_p), ("V", ctypes.c_void_p),
@@ -59,7 +72,7 @@ class StepArgs(ctypes.Structure):
                 ("g", ctypes.c_double),
                 ("dt_bound", ctypes.c_void_p), ("cfl", ctypes.c_double),
                 ("bc", ctypes.c_int32 * 4), ("mode", ctypes.c_int32), ("variant", ctypes.c_int32),
-                ("red", Reduce)]
+                ("red", Reduce), ("peer", PeerLine * 4), ("sync", Sync)]
 
 
 _lib = None
@@ -96,6 +109,9 @@ def lib():
         "fkc_copy2d": [vp, i64, vp, i64, i64, i64, vp],
         "fkc_halo_pack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
         "fkc_halo_unpack": [ctypes.POINTER(Grid), vp, vp, vp, i32, vp, vp],
+        "fkc_ipc_export": [vp, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(i64)],
+        "fkc_ipc_open": [ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(vp)],
+        "fkc_ipc_close": [vp],
         "fkc_set_tma_segment": [ctypes.c_int],
         "fkc_test_div_f32": [vp, vp, vp, vp, i64, vp],
         "fkc_abi_version": [],
@@ -107,6 +123,25 @@ def lib():
         fn.restype = ctypes.c_char_p if name == "fkc_last_error" else ctypes.c_int
     _lib = L
     return L
+
+
+def ipc_export(ptr: int):
+    """(64-byte handle, byte offset of ptr in its allocation)."""
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_int64()
+    check(lib().fkc_ipc_export(ptr, h, ctypes.byref(off)))
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    base = ctypes.c_void_p()
+    check(lib().fkc_ipc_open(h, ctypes.byref(base)))
+    return base.value
+
+
+def ipc_close(base: int):
+    check(lib().fkc_ipc_close(base))
 
 
 def check(rc: int):

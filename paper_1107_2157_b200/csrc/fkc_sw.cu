@@ -67,6 +67,50 @@ RedPtrs to_red(const fkc_sw_reduce& r) {
 
 bool any_red(const RedPtrs& p) { return p.mass || p.max_u || p.max_v || p.cfl_min || p.err; }
 
+Peers to_peers(const fkc_sw_step_args* a) {
+    Peers P;
+    for (int s = 0; s < 4; ++s) {
+        for (int f = 0; f < 3; ++f) P.s[s].p[f] = a->peer[s].p[0] ? a->peer[s].p[f] : nullptr;
+        P.s[s].stride = a->peer[s].stride;
+    }
+    return P;
+}
+
+SyncArgs to_sync(const fkc_sw_step_args* a) {
+    SyncArgs S;
+    for (int s = 0; s < 4; ++s) {
+        S.wait[s] = a->sync.wait[s];
+        S.signal[s] = a->sync.signal[s];
+    }
+    S.counter = a->sync.counter;
+    S.epoch = a->sync.epoch;
+    return S;
+}
+
+int valid_peers(const fkc_sw_step_args* a) {
+    for (int s = 0; s < 4; ++s) {
+        const fkc_peer_line& l = a->peer[s];
+        if (!l.p[0]) continue;
+        if (!l.p[1] || !l.p[2]) return fail(FKC_EUSAGE, "peer line %d: null field pointer", s);
+        if (a->bc[s] != FKC_BC_NONE) return fail(FKC_EUSAGE, "peer line %d needs bc NONE on that side", s);
+        if (s >= 2 ? l.stride != 1 : l.stride < (int64_t)1) return fail(FKC_EUSAGE, "peer line %d: bad stride", s);
+    }
+    const fkc_sync& y = a->sync;
+    if (y.counter) {
+        for (int s = 0; s < 4; ++s)
+            if ((y.wait[s] != nullptr) != (y.signal[s] != nullptr))
+                return fail(FKC_EUSAGE, "sync side %d: wait and signal must be given together", s);
+    }
+    return FKC_OK;
+}
+
+bool peers_tma_ok(const fkc_sw_step_args* a) {
+    for (int s = 2; s < 4; ++s)
+        for (int f = 0; f < 3; ++f)
+            if (a->peer[s].p[0] && (((uintptr_t)a->peer[s].p[f]) + 4) % 16 != 0) return false;
+    return true;
+}
+
 // ---------------------------------------------------------------------------
 // TMA tensor maps (driver entry point fetched through the runtime so the
 // library does not link libcuda directly)
@@ -140,7 +184,7 @@ bool tma_eligible(const fkc_sw_step_args* a) {
     const void* ps[6] = {a->H, a->U, a->V, a->oH, a->oU, a->oV};
     for (const void* p : ps)
         if ((((uintptr_t)p) + 4) % 16 != 0) return false;
-    return true;
+    return peers_tma_ok(a);
 }
 
 template <class T>
@@ -153,7 +197,7 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(red);
 #define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
-                 (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red
+                 (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red, to_peers(a), to_sync(a)
     if (fast) {
         if (r) sw_step_generic<T, DIV_FAST, true><<<grd, blk, 0, st>>>(GEN_ARGS);
         else sw_step_generic<T, DIV_FAST, false><<<grd, blk, 0, st>>>(GEN_ARGS);
@@ -197,7 +241,8 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
     kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
                                                    (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
-                                                   dts, (float)a->g, to_bcs(a->bc), to_red(a->red));
+                                                   dts, (float)a->g, to_bcs(a->bc), to_red(a->red),
+                                                   to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
 }
 
@@ -251,12 +296,14 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (!valid_bc(a->bc)) return fail(FKC_EUSAGE, "invalid boundary spec");
     if (a->mode != FKC_MODE_EXACT && a->mode != FKC_MODE_FAST) return fail(FKC_EUSAGE, "invalid mode");
     if (!(a->dx > 0) || !(a->dy > 0)) return fail(FKC_EUSAGE, "dx, dy must be > 0");
+    if (int rc = valid_peers(a)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     int variant = a->variant;
     if (variant == FKC_VARIANT_AUTO) variant = tma_eligible(a) ? FKC_VARIANT_TMA : FKC_VARIANT_GENERIC;
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
-            return fail(FKC_EUSAGE, "TMA variant needs f32, nx%%4==0, pitch%%4==0 and (ptr+1) 16-B aligned");
+            return fail(FKC_EUSAGE, "TMA variant needs f32, nx%%4==0, pitch%%4==0 and (ptr+1) 16-B aligned "
+                                    "(fields and row peer lines)");
         return launch_tma(a, st);
     }
     if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");
@@ -381,6 +428,47 @@ int fkc_halo_pack(const fkc_grid* g, const void* H, const void* U, const void* V
                   void* stream) {
     if (!H || !U || !V || !buf) return fail(FKC_EUSAGE, "null pointer");
     return halo_common(g, side, false, H, U, V, buf, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int fkc_ipc_export(const void* ptr, uint8_t handle[64], int64_t* offset) {
+    if (!ptr || !handle || !offset) return fail(FKC_EUSAGE, "null pointer");
+    typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range = (RangeFn)p;
+    });
+    if (!range) return fail(FKC_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(FKC_EUSAGE, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, 64);
+    *offset = (int64_t)((CUdeviceptr)ptr - base);
+    return FKC_OK;
+}
+
+int fkc_ipc_open(const uint8_t handle[64], void** base) {
+    if (!handle || !base) return fail(FKC_EUSAGE, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return FKC_OK;
+}
+
+int fkc_ipc_close(void* base) {
+    if (!base) return fail(FKC_EUSAGE, "null pointer");
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return FKC_OK;
 }
 
 int fkc_halo_unpack(const fkc_grid* g, void* H, void* U, void* V, int32_t side, const void* buf, void* stream) {

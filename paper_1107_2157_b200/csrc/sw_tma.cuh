@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::template ctas_per
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg,
             float* __restrict__ oH, float* __restrict__ oU, float* __restrict__ oV,
-            float dx, float dy, DtSrc dts, float g, BCs bc, RedPtrs red) {
+            float dx, float dy, DtSrc dts, float g, BCs bc, RedPtrs red, Peers P, SyncArgs sy) {
     using namespace tma;
     using G = Geo<CPL>;
     // CPL = 4 keeps every TMA box start (tensor column 120 j) 16-byte aligned;
@@ -193,12 +193,21 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
     const int nstages = (nload + R - 1) / R;
     const uint32_t ring = sbase + warp * G::WARP_RING;
-    const uint32_t full = sbase + WARPS * G::WARP_RING + warp * S * 8;
+    const uint32_t full = sbase + WARPS * G::WARP_RING + warp * tma::S * 8;
 
+    // tile sides this warp exchanges with neighbour tiles (fused halo exchange)
+    uint32_t sides = 0;
+    if (sync_on(sy)) {
+        if (y0 == 1) sides |= 1u << SIDE_D;
+        if (y0 + nrows - 1 == ny) sides |= 1u << SIDE_U;
+        if (strip == 0) sides |= 1u << SIDE_L;
+        if (G::OWN * (strip + 1) >= nx) sides |= 1u << SIDE_R;
+    }
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(full + 8 * s, 1);
+        if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
+        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < S - 1 && k < nstages; ++k)
+        for (int k = 0; k < tma::S - 1 && k < nstages; ++k)
             issue_stage<CPL>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, y0 - 1 + k * R);
     }
     __syncwarp();
@@ -230,15 +239,15 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     constexpr int UNR = FAST ? R : FKC_EXACT_UNROLL;  // exact: keep the loop body inside the I-cache
 
     for (int k = 0; k < nstages; ++k) {
-        const int s = k % S;
+        const int s = k % tma::S;
         // refill the slot freed by stage k-1 (every lane finished reading it)
-        if (lane == 0 && k + S - 1 < nstages) {
-            const int kn = k + S - 1;
+        if (lane == 0 && k + tma::S - 1 < nstages) {
+            const int kn = k + tma::S - 1;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_stage<CPL>(ring + (kn % S) * G::STAGE_BYTES, full + 8 * (kn % S), &tmH, &tmU, &tmV, tx,
+            issue_stage<CPL>(ring + (kn % tma::S) * G::STAGE_BYTES, full + 8 * (kn % tma::S), &tmH, &tmU, &tmV, tx,
                              y0 - 1 + kn * R);
         }
-        mbar_wait(full + 8 * s, (k / S) & 1, red.err);
+        mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
         const uint32_t st = ring + s * G::STAGE_BYTES + lane_off;
 #pragma unroll UNR
         for (int r = 0; r < R; ++r) {
@@ -307,13 +316,31 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                             stg_vec<CPL>(oU + o2, ou);
                             stg_vec<CPL>(oV + o2, ov);
                         }
+                        // fused halo exchange: the new row goes straight into
+                        // the neighbour tile's halo row (rows: stride 1)
+                        const PeerLine& pl = P.s[y == 1 ? SIDE_D : SIDE_U];
+                        if (pl.p[0]) {
+                            stg_vec<CPL>((float*)pl.p[0] + X, oh);
+                            stg_vec<CPL>((float*)pl.p[1] + X, ou);
+                            stg_vec<CPL>((float*)pl.p[2] + X, ov);
+                        }
+                        if (y == 1 && y == ny && P.s[SIDE_U].p[0]) {   // single-row tile
+                            stg_vec<CPL>((float*)P.s[SIDE_U].p[0] + X, oh);
+                            stg_vec<CPL>((float*)P.s[SIDE_U].p[1] + X, ou);
+                            stg_vec<CPL>((float*)P.s[SIDE_U].p[2] + X, ov);
+                        }
                     }
                     if (edge_cols) {
-                        if (X == 1)
+                        if (X == 1) {
                             emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, 1, y, oh[0], ou[0], ov[0], false);
-                        if (X + CPL - 1 == nx)
+                            if (P.s[SIDE_L].p[0]) peer_store<float>(P.s[SIDE_L], y, oh[0], ou[0], ov[0]);
+                        }
+                        if (X + CPL - 1 == nx) {
                             emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, nx, y, oh[CPL - 1], ou[CPL - 1],
                                               ov[CPL - 1], false);
+                            if (P.s[SIDE_R].p[0])
+                                peer_store<float>(P.s[SIDE_R], y, oh[CPL - 1], ou[CPL - 1], ov[CPL - 1]);
+                        }
                     }
                     if (RED) {
                         double m = 0.0;
@@ -332,6 +359,13 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             pxl = nxl;
         }
         __syncwarp();
+    }
+    if (sides) {
+        __threadfence_system();
+        __syncwarp();
+        const int nstrips = (nx - 1) / G::OWN + 1;
+        const int expected[4] = {(int)gridDim.y, (int)gridDim.y, nstrips, nstrips};
+        if (lane == 0) peer_signal(sy, sides, expected);
     }
     if (RED) warp_reduce_commit<float>(acc, red, lane);
 }

@@ -255,6 +255,135 @@ class LocalTransport:
 
 
 # ---------------------------------------------------------------------------
+# fused exchange: the step kernel stores boundary lines into the neighbours'
+# halos (peer memory) and orders steps with mailbox words -- no separate
+# pack / transfer / unpack phase (include/fkc_sw.h fkc_peer_line, fkc_sync)
+# ---------------------------------------------------------------------------
+
+def set_peer_line(line: "N.PeerLine", side: int, ptrs: Sequence[int], pitch: int, nbr_nx: int, nbr_ny: int,
+                  itemsize: int):
+    """Fill `line` so that our boundary cells land in the halo of the
+    neighbour across `side`, whose fields (element (0,0) at ptrs[f]) have row
+    pitch `pitch` and interior nbr_nx x nbr_ny: our row 1 -> its row ny+1
+    (down), row ny -> row 0 (up), column 1 -> column nx+1 (left), column
+    nx -> column 0 (right)."""
+    if side == DOWN:
+        off, stride = (nbr_ny + 1) * pitch, 1
+    elif side == UP:
+        off, stride = 0, 1
+    elif side == LEFT:
+        off, stride = nbr_nx + 1, pitch
+    else:
+        off, stride = 0, pitch
+    for f in range(3):
+        line.p[f] = ptrs[f] + off * itemsize
+    line.stride = stride
+
+
+def _field_ptrs(st) -> Tuple[int, int, int]:
+    return st.H.ptr, st.U.ptr, st.V.ptr
+
+
+class Mailbox:
+    """Per-tile sync words: [0..3] mailbox per side (written by that side's
+    neighbour), [4..7] edge-writer counters (used by the kernel)."""
+
+    def __init__(self, device):
+        import torch
+        self.buf = torch.zeros(8, dtype=torch.int32, device=device)
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def word(self, side: int) -> int:
+        return self.ptr + 4 * side
+
+    @property
+    def counters(self) -> int:
+        return self.ptr + 16
+
+
+def fill_sync(sync: "N.Sync", mail: Mailbox, signal: Dict[int, int], epoch: int):
+    """wait on our own mailbox words, signal the neighbours' words for us."""
+    for s in (LEFT, RIGHT, DOWN, UP):
+        if s in signal:
+            sync.wait[s] = mail.word(s)
+            sync.signal[s] = signal[s]
+        else:
+            sync.wait[s] = None
+            sync.signal[s] = None
+    sync.counter = mail.counters
+    sync.epoch = epoch & 0xFFFFFFFF
+
+
+def initial_peer_exchange(grid: CartGrid, rank: int, st, lines: Dict[int, "N.PeerLine"], stream=None):
+    """One-time fill of the neighbours' halos of their INITIAL buffers from
+    our initial boundary lines (pitched DMA through peer memory, fkc_copy2d)."""
+    import torch
+    t = grid.tile(rank)
+    it = st.H.storage.element_size()
+    sp = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+    L = N.lib()
+    for side, line in lines.items():
+        for f, fld in enumerate((st.H, st.U, st.V)):
+            p = fld.pitch
+            if side in (DOWN, UP):
+                y = 1 if side == DOWN else t.ny
+                src = fld.ptr + (y * p + 1) * it
+                N.check(L.fkc_copy2d(line.p[f] + it, t.nx * it, src, t.nx * it, t.nx * it, 1, sp))
+            else:
+                x = 1 if side == LEFT else t.nx
+                src = fld.ptr + (p + x) * it
+                N.check(L.fkc_copy2d(line.p[f] + line.stride * it, line.stride * it, src, p * it, it, t.ny, sp))
+
+
+class PeerExchange:
+    """Fused exchange between the processes of a decomposed run (one per
+    GPU): every rank exports its two state buffers (H,U,V of each parity) and
+    its mailbox with CUDA IPC, opens its neighbours' (NVLink / NVSwitch peer
+    memory), and from then on the step kernel itself writes the neighbours'
+    halos and signals their mailboxes."""
+
+    def __init__(self, grid: CartGrid, rank: int, bufs, group=None):
+        import torch.distributed as dist
+        self.grid, self.rank = grid, rank
+        dev = bufs[0].H.storage.device
+        self.mail = Mailbox(dev)
+        mine = {"bufs": [[N.ipc_export(p) for p in _field_ptrs(b)] for b in bufs],
+                "mail": N.ipc_export(self.mail.ptr),
+                "pitch": bufs[0].H.pitch, "itemsize": bufs[0].H.storage.element_size()}
+        everyone = [None] * dist.get_world_size(group)
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened: Dict[bytes, int] = {}
+        self.nbr = {s: grid.neighbor(rank, s) for s in (LEFT, RIGHT, DOWN, UP)}
+        self.nbr = {s: n for s, n in self.nbr.items() if n is not None}
+        # lines[p][side]: targets for a step whose OUTPUT parity is p
+        self.lines = [{}, {}]
+        self.signal: Dict[int, int] = {}
+        for s, n in self.nbr.items():
+            info = everyone[n]
+            nt = grid.tile(n)
+            for p in (0, 1):
+                ptrs = [self._open(h) + off for h, off in info["bufs"][p]]
+                line = N.PeerLine()
+                set_peer_line(line, s, ptrs, info["pitch"], nt.nx, nt.ny, info["itemsize"])
+                self.lines[p][s] = line
+            h, off = info["mail"]
+            self.signal[s] = self._open(h) + off + 4 * OPPOSITE[s]
+
+    def _open(self, handle: bytes) -> int:
+        if handle not in self._opened:
+            self._opened[handle] = N.ipc_open(handle)
+        return self._opened[handle]
+
+    def close(self):
+        for base in self._opened.values():
+            N.ipc_close(base)
+        self._opened.clear()
+
+
+# ---------------------------------------------------------------------------
 # initial state of a tile (same f64 formula as swdemo.init_state)
 # ---------------------------------------------------------------------------
 
@@ -284,10 +413,15 @@ class DistributedSimulation:
     runs the per-rank bound from the fused reduction is all-reduced (MIN).
     """
 
-    def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None):
+    def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None,
+                 transport: str = "peer"):
         import torch
+        import torch.distributed as dist
         from . import swdemo
         from .field import DeviceField, Field
+        if transport not in ("peer", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
         self.cfg, self.grid, self.rank = cfg, grid, rank
         self.tile = grid.tile(rank)
         self.bc = grid.local_bc(rank)
@@ -303,32 +437,77 @@ class DistributedSimulation:
         self.a = st
         self.b = swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx, st.dy)
         tdt = torch.float32 if cfg.precision == "f32" else torch.float64
-        self.ex = HaloExchanger(grid, rank, DistTransport(group), NativeLines(stream), st.H.storage.device, tdt)
         swdemo.apply_boundary(self.a, self.bc, stream)
-        self.ex.exchange(self.a)
         self.n = 0
+        self.ex = self.peer = None
+        if transport == "nccl":
+            self.ex = HaloExchanger(grid, rank, DistTransport(group), NativeLines(stream), st.H.storage.device,
+                                    tdt)
+            self.ex.exchange(self.a)
+        else:
+            self.peer = PeerExchange(grid, rank, (self.a, self.b), group)
+            initial_peer_exchange(grid, rank, self.a, self.peer.lines[0], stream)
+            (stream or torch.cuda.current_stream()).synchronize()
+            dist.barrier(group)
+        self._group = group
+
+    def _launches_per_step(self) -> int:
+        return 1 if self.transport == "peer" else 1 + 2 * len(self.ex.send)
 
     def advance(self, steps: int):
         from . import swdemo
+        L = N.lib()
+        sp = swdemo._stream_ptr(self.stream)
         for _ in range(steps):
             src, dst = (self.a, self.b) if self.n % 2 == 0 else (self.b, self.a)
-            swdemo.advance(src, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant, out=dst,
-                           stream=self.stream)
-            self.ex.exchange(dst)
+            if self.transport == "peer":
+                a = swdemo._step_args(src, dst, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant)
+                out_parity = (self.n + 1) % 2
+                for s, line in self.peer.lines[out_parity].items():
+                    a.peer[s] = line
+                fill_sync(a.sync, self.peer.mail, self.peer.signal, self.n)
+                N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+                dst.t = src.t + float(self.cfg.dt)
+            else:
+                swdemo.advance(src, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant, out=dst,
+                               stream=self.stream)
+                self.ex.exchange(dst)
             self.n += 1
         return self
+
+    def close(self):
+        """Drain, then unmap the neighbours' memory (collective)."""
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        dist.barrier(self._group)
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
+        dist.barrier(self._group)
 
     def state(self):
         return self.a if self.n % 2 == 0 else self.b
 
 
-def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None):
-    """All px*py tiles in one process on one device (LocalTransport): the
-    GPU-side validation of the decomposed path.  Returns the tiles' states."""
+def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchange: str = "pack",
+                         concurrent: bool = False):
+    """All px*py tiles in one process on one device: the GPU-side validation
+    of the decomposed path.  Returns (grid, the tiles' states).
+
+    exchange="pack": step kernel, then native line pack / copy / unpack
+    (LocalTransport).  exchange="fused": the step kernel writes the
+    neighbours' halos itself (peer lines into the other tiles' buffers); with
+    concurrent=True every tile runs on its own stream and steps are ordered
+    only by the in-kernel mailbox protocol -- the multi-GPU synchronisation,
+    exercised on one device."""
+    import torch
     from . import swdemo
     from .field import Field
+    if exchange not in ("pack", "fused"):
+        raise ValueError(f"unknown exchange {exchange!r}")
     grid = CartGrid(px, py, cfg.nx, cfg.ny, cfg.boundary)
-    states, others, exs = [], [], []
+    bufs = []        # bufs[r] = (parity-0 state, parity-1 state)
     for r in range(grid.size):
         t = grid.tile(r)
         full = Extent(t.nx + 2, t.ny + 2)
@@ -338,20 +517,58 @@ def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None):
         st = swdemo.SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
                             cfg.g, cfg.dx, cfg.dy).to_device(device)
         swdemo.apply_boundary(st, grid.local_bc(r))
-        states.append(st)
-        others.append(swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx,
-                                     st.dy))
-        import torch
-        exs.append(HaloExchanger(grid, r, None, NativeLines(), st.H.storage.device,
-                                 torch.float32 if cfg.precision == "f32" else torch.float64))
-    lt = LocalTransport(grid)
-    lt.exchange_all(exs, states)
-    for _ in range(steps):
-        for r in range(grid.size):
-            swdemo.advance(states[r], cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant, out=others[r])
-        states, others = others, states
+        bufs.append((st, swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx,
+                                        st.dy)))
+    tdt = torch.float32 if cfg.precision == "f32" else torch.float64
+    if exchange == "pack":
+        states, others = [b[0] for b in bufs], [b[1] for b in bufs]
+        exs = [HaloExchanger(grid, r, None, NativeLines(), states[r].H.storage.device, tdt)
+               for r in range(grid.size)]
+        lt = LocalTransport(grid)
         lt.exchange_all(exs, states)
-    return grid, states
+        for _ in range(steps):
+            for r in range(grid.size):
+                swdemo.advance(states[r], cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant, out=others[r])
+            states, others = others, states
+            lt.exchange_all(exs, states)
+        return grid, states
+
+    dev = bufs[0][0].H.storage.device
+    lines = []       # lines[r][p][side]
+    for r in range(grid.size):
+        per = [{}, {}]
+        for s in (LEFT, RIGHT, DOWN, UP):
+            n = grid.neighbor(r, s)
+            if n is None:
+                continue
+            nt = grid.tile(n)
+            for p in (0, 1):
+                nb = bufs[n][p]
+                line = N.PeerLine()
+                set_peer_line(line, s, _field_ptrs(nb), nb.H.pitch, nt.nx, nt.ny, nb.H.storage.element_size())
+                per[p][s] = line
+        lines.append(per)
+    for r in range(grid.size):
+        initial_peer_exchange(grid, r, bufs[r][0], lines[r][0])
+    torch.cuda.synchronize()
+    mails = [Mailbox(dev) for _ in range(grid.size)] if concurrent else None
+    streams = [torch.cuda.Stream(dev) for _ in range(grid.size)] if concurrent else None
+    L = N.lib()
+    for k in range(steps):
+        for r in range(grid.size):
+            src, dst = bufs[r][k % 2], bufs[r][(k + 1) % 2]
+            a = swdemo._step_args(src, dst, cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant)
+            for s, line in lines[r][(k + 1) % 2].items():
+                a.peer[s] = line
+            if concurrent:
+                sig = {s: mails[grid.neighbor(r, s)].word(OPPOSITE[s]) for s in lines[r][0]}
+                fill_sync(a.sync, mails[r], sig, k)
+                sp = streams[r].cuda_stream
+            else:
+                sp = torch.cuda.current_stream(dev).cuda_stream
+            N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+    torch.cuda.synchronize()
+    return grid, [b[steps % 2] for b in bufs]
 
 
 def gather_interior(grid: CartGrid, tiles: Sequence[np.ndarray]) -> np.ndarray:
@@ -388,7 +605,7 @@ def bench_main(args, rank: int, world: int) -> int:
     cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
-        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream)
+        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport)
         sim.advance(args.warmup)
         torch.cuda.synchronize()
         dist.barrier()
@@ -412,12 +629,16 @@ def bench_main(args, rank: int, world: int) -> int:
                 "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
                 "config": {"workload": f"shallow-water {n}x{n} fp32 per GPU, 2-D decomposed {px}x{py}, "
-                                       "one-cell halo exchange per step (NCCL P2P)",
+                                       "one-cell halo exchange per step " +
+                                       ("fused into the step kernel (NVLink peer stores + mailbox flags)"
+                                        if args.transport == "peer" else "(pack + NCCL send/recv + unpack)"),
+                           "transport": args.transport,
                            "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
                 "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
                              "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
-                "gpu_launches": args.steps * (1 + 2 * len(sim.ex.send))}
+                "gpu_launches": args.steps * sim._launches_per_step()}
         print(json.dumps(line))
+    sim.close()
     dist.destroy_process_group()
     return 0

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(N.EXPORTS), (names, N.EXPORTS)
     for name in names:
         assert hasattr(L, name), name
-    assert L.fkc_abi_version() == 1
+    assert L.fkc_abi_version() == N.ABI_VERSION == 2
 
 
 def test_usage_errors_without_gpu():
@@ -44,6 +44,23 @@ def test_usage_errors_without_gpu():
     halo = (ctypes.c_int32 * 4)(3, 3, 0, 0)
     assert L.fkc_region_cpy(0, 16, 5, 5, 5, halo, 32, 5, None) == N.FKC_EDOMAIN  # HaloTooLarge
     assert L.fkc_set_tma_segment(-1) == N.FKC_EUSAGE
+    # fused exchange: a peer line needs bc NONE on its side, and wait/signal come in pairs
+    a.grid = N.Grid(8, 8, 12, 0, 0)
+    a.H, a.U, a.V, a.oH, a.oU, a.oV = 1024, 2048, 3072, 4096, 5120, 6144
+    a.dx = a.dy = 1.0
+    a.peer[2].p[0] = a.peer[2].p[1] = a.peer[2].p[2] = 8192
+    a.peer[2].stride = 1
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    assert b"NONE" in L.fkc_last_error()
+    a.bc[2] = N.BC_NONE
+    a.peer[2].stride = 7
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    assert b"stride" in L.fkc_last_error()
+    a.peer[2].stride = 1
+    a.sync.counter = 1 << 20
+    a.sync.wait[0] = 1 << 21
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    assert b"together" in L.fkc_last_error()
 
 
 def test_struct_layout_matches_header():
@@ -56,6 +73,9 @@ def test_struct_layout_matches_header():
       printf("%zu %zu %zu %zu %zu %zu\n", offsetof(fkc_sw_step_args, H), offsetof(fkc_sw_step_args, dx),
              offsetof(fkc_sw_step_args, dt_bound), offsetof(fkc_sw_step_args, bc),
              offsetof(fkc_sw_step_args, variant), offsetof(fkc_sw_step_args, red));
+      printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_peer_line), sizeof(fkc_sync),
+             offsetof(fkc_sw_step_args, peer), offsetof(fkc_sw_step_args, sync),
+             offsetof(fkc_sync, counter), offsetof(fkc_sync, epoch));
       return 0;
     }
     """
@@ -68,7 +88,9 @@ def test_struct_layout_matches_header():
     got = list(map(int, out))
     S = N.StepArgs
     want = [ctypes.sizeof(N.Grid), ctypes.sizeof(N.Reduce), ctypes.sizeof(S),
-            S.H.offset, S.dx.offset, S.dt_bound.offset, S.bc.offset, S.variant.offset, S.red.offset]
+            S.H.offset, S.dx.offset, S.dt_bound.offset, S.bc.offset, S.variant.offset, S.red.offset,
+            ctypes.sizeof(N.PeerLine), ctypes.sizeof(N.Sync), S.peer.offset, S.sync.offset,
+            N.Sync.counter.offset, N.Sync.epoch.offset]
     assert got == want
 
 

@@ -141,15 +141,153 @@ def test_gloo_decomposed_bit_identical(px, py, bc):
 @pytest.mark.parametrize("px,py", [(1, 2), (2, 2), (2, 4)])
 @pytest.mark.parametrize("bc", ["reflective", "periodic"])
 @pytest.mark.parametrize("mode", ["exact", "fast"])
-def test_local_decomposed_gpu_bit_identical(px, py, bc, mode):
-    """px*py tiles on one GPU (native kernels, per-side BC, native line
-    pack/unpack) == the single-domain GPU run, bit for bit (fast mode
-    included: the decomposition does not change per-cell arithmetic)."""
+@pytest.mark.parametrize("exchange", ["pack", "fused", "fused-concurrent"])
+def test_local_decomposed_gpu_bit_identical(px, py, bc, mode, exchange):
+    """px*py tiles on one GPU (native kernels, per-side BC) == the
+    single-domain GPU run, bit for bit (fast mode included: the
+    decomposition does not change per-cell arithmetic).  pack: native line
+    pack / copy / unpack; fused: the step kernel stores its boundary lines
+    into the neighbours' halos; fused-concurrent: every tile on its own
+    stream, ordered only by the in-kernel mailbox protocol."""
     from paper_1107_2157_b200 import swdemo
     from paper_1107_2157_b200.decomp import run_local_decomposed
     nx, ny, steps = 960, 512, 8
     cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode)
-    grid, states = run_local_decomposed(cfg, px, py, steps)
+    grid, states = run_local_decomposed(cfg, px, py, steps, exchange=exchange.split("-")[0],
+                                        concurrent=exchange.endswith("concurrent"))
+    sim = swdemo.Simulation(cfg, diagnostics=False)
+    sim.advance(steps)
+    ref = sim.state()
+    for f in ("H", "U", "V"):
+        got = gather_interior(grid, [getattr(s, f).to_numpy()[1:-1, 1:-1] for s in states])
+        assert np.array_equal(got, getattr(ref, f).to_numpy()[1:-1, 1:-1]), f
+
+
+# ---------------------------------------------------------------------------
+# fused exchange (the step kernel writes the neighbours' halos)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 2), (2, 4)])
+@pytest.mark.parametrize("bc", ["reflective", "periodic"])
+def test_peer_line_addressing(px, py, bc):
+    """CPU tier: the peer-line addresses map every boundary cell of a tile
+    onto exactly the neighbour halo cell the pack/unpack exchange fills.
+    Fake 'device memory': each tile's field f lives at base(r, f) with
+    pitch nx+7; decode the kernel's store address back to (tile, field, x, y)."""
+    from paper_1107_2157_b200 import _native as N
+    from paper_1107_2157_b200.decomp import OPPOSITE, set_peer_line
+    g = CartGrid(px, py, 44, 36, bc)
+    it = 4
+    span = 1 << 24
+
+    def base(r, f):
+        return (1 + 3 * r + f) * span
+
+    def pitch(r):
+        return g.tile(r).nx + 7
+
+    def decode(addr):
+        k, off = divmod(addr, span)
+        r, f = divmod(k - 1, 3)
+        y, x = divmod(off // it, pitch(r))
+        return r, f, x, y
+
+    for r in range(g.size):
+        t = g.tile(r)
+        for s in (LEFT, RIGHT, DOWN, UP):
+            n = g.neighbor(r, s)
+            if n is None:
+                continue
+            nt = g.tile(n)
+            line = N.PeerLine()
+            set_peer_line(line, s, [base(n, f) for f in range(3)], pitch(n), nt.nx, nt.ny, it)
+            # the cells the kernel stores for this side, and where they must land
+            if s in (DOWN, UP):
+                y = 1 if s == DOWN else t.ny
+                cells = [(x, y) for x in range(1, t.nx + 1)]
+                want = [(x, nt.ny + 1 if s == DOWN else 0) for x, _ in cells]
+                idx = [x for x, _ in cells]
+            else:
+                x = 1 if s == LEFT else t.nx
+                cells = [(x, y) for y in range(1, t.ny + 1)]
+                want = [(nt.nx + 1 if s == LEFT else 0, y) for _, y in cells]
+                idx = [y for _, y in cells]
+            for f in range(3):
+                got = [decode(line.p[f] + i * line.stride * it) for i in idx]
+                assert all(gr == n and gf == f for gr, gf, _, _ in got)
+                assert [(gx, gy) for _, _, gx, gy in got] == want
+            # and the neighbour fills its OPPOSITE halo side from us
+            assert g.neighbor(n, OPPOSITE[s]) == r
+
+
+def _peer_worker(rank, world, port, px, py, nx, ny, steps, bc, mode, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.decomp import DistributedSimulation
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        grid = CartGrid(px, py, nx, ny, bc)
+        cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode)
+        sim = DistributedSimulation(cfg, grid, rank, torch.device("cuda", 0), transport="peer")
+        sim.advance(steps)
+        torch.cuda.synchronize()
+        st = sim.state()
+        q.put((rank, *(getattr(st, f).to_numpy()[1:-1, 1:-1] for f in ("H", "U", "V"))))
+        sim.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("px,py,bc", [(1, 2, "reflective"), (2, 2, "periodic")])
+def test_ipc_peer_processes_bit_identical(px, py, bc):
+    """One process per tile, all on cuda:0: CUDA-IPC peer memory, the fused
+    in-kernel exchange and the mailbox ordering across processes (what runs
+    across GPUs over NVLink) == the single-domain run, bit for bit."""
+    import torch.multiprocessing as mp
+
+    from paper_1107_2157_b200 import swdemo
+    world = px * py
+    nx, ny, steps = 960, 512, 10
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, px, py, nx, ny, steps, bc, "exact", q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, h, u, v = q.get(timeout=300)
+        res[r] = (h, u, v)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    grid = CartGrid(px, py, nx, ny, bc)
+    cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode="exact")
+    sim = swdemo.Simulation(cfg, diagnostics=False)
+    sim.advance(steps)
+    ref = sim.state()
+    for k, f in enumerate(("H", "U", "V")):
+        got = gather_interior(grid, [res[r][k] for r in range(world)])
+        assert np.array_equal(got, getattr(ref, f).to_numpy()[1:-1, 1:-1]), f
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_local_fused_generic_kernel(precision):
+    """The generic (one thread per cell) kernel's fused exchange and CTA-level
+    mailbox protocol: odd tile widths (no TMA) and f64, concurrent streams."""
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.decomp import run_local_decomposed
+    nx, ny, steps = 331, 203, 7
+    cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary="periodic", mode="exact", precision=precision)
+    grid, states = run_local_decomposed(cfg, 2, 2, steps, exchange="fused", concurrent=True)
     sim = swdemo.Simulation(cfg, diagnostics=False)
     sim.advance(steps)
     ref = sim.state()
