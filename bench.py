@@ -166,7 +166,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=16384, help="cells per side (per GPU)")
+    ap.add_argument("--n", "--grid-n", dest="n", type=int, default=16384, help="cells per side (per GPU)")
     ap.add_argument("--mode", default="fast", choices=["exact", "fast"],
                     help="fast: FMA + approximate reciprocals, rtol 2e-5 vs the oracle (headline); "
                          "exact: bit-identical to the oracle")

@@ -594,9 +594,18 @@ def bench_main(args, rank: int, world: int) -> int:
     from . import swdemo
 
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # FKC_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo host collectives
+    # -- exercises the N>1 code path (IPC peer memory, mailboxes) on a
+    # one-GPU box; its timings are meaningless (time-sliced contexts)
+    one_dev = os.environ.get("FKC_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if one_dev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     px, py = choose_grid(world)
     n = args.n
     grid = CartGrid(px, py, px * n, py * n, "reflective")
@@ -615,7 +624,7 @@ def bench_main(args, rank: int, world: int) -> int:
         t1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    ms = torch.tensor([t0.elapsed_time(t1)], device="cpu" if one_dev else dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
     cells = grid.NX * grid.NY
