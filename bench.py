@@ -172,6 +172,8 @@ def main():
                          "exact: bit-identical to the oracle")
     ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
     ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
+    ap.add_argument("--alt", type=int, default=1, choices=[0, 1],
+                    help="TMA kernel: odd segments sweep top-down (L2 reuse of shared halo rows)")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1 halo exchange: peer = fused into the step kernel over NVLink peer memory "
                          "(CUDA IPC + mailbox flags); nccl = pack + NCCL send/recv + unpack (baseline)")
@@ -218,6 +220,7 @@ def main():
     dev = torch.device("cuda", 0)
     if args.seg:
         N.check(N.lib().fkc_set_tma_segment(args.seg))
+    N.check(N.lib().fkc_set_tma_alternate(args.alt))
     st = device_gaussian_state(n, n, dev)
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0

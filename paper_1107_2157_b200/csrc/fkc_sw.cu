@@ -210,6 +210,7 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
 }
 
 int g_seg_override = 0;
+int g_alt = 1;   // alternate the sweep direction of odd segments (L2 reuse of shared halo rows)
 
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
@@ -239,7 +240,7 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const int seg = pick_seg(nbands, g.ny, G::template ctas_per_sm<FAST>());
     dim3 grd(nbands, (g.ny + seg - 1) / seg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, (float*)a->oH,
+    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, g_alt, (float*)a->oH,
                                                    (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
                                                    dts, (float)a->g, to_bcs(a->bc), to_red(a->red),
                                                    to_peers(a), to_sync(a));
@@ -276,6 +277,13 @@ int fkc_abi_version(void) { return FKC_ABI_VERSION; }
 int fkc_set_tma_segment(int seg) {
     if (seg < 0) return fail(FKC_EUSAGE, "segment must be >= 0");
     g_seg_override = seg;
+    return FKC_OK;
+}
+
+// test hook: alternate the TMA kernel's sweep direction per segment (1, default) or not (0)
+int fkc_set_tma_alternate(int on) {
+    if (on != 0 && on != 1) return fail(FKC_EUSAGE, "alternate must be 0 or 1");
+    g_alt = on;
     return FKC_OK;
 }
 

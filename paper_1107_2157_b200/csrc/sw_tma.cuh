@@ -170,7 +170,7 @@ __device__ __forceinline__ void row_faces(const VecF<CPL>& h, const VecF<CPL>& u
 template <int CPL, bool FAST, bool RED>
 __global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::template ctas_per_sm<FAST>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
-            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg,
+            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg, int alt,
             float* __restrict__ oH, float* __restrict__ oU, float* __restrict__ oV,
             float dx, float dy, DtSrc dts, float g, BCs bc, RedPtrs red, Peers P, SyncArgs sy) {
     using namespace tma;
@@ -192,6 +192,21 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int nrows = min(seg, ny - y0 + 1);
     const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
     const int nstages = (nload + R - 1) / R;
+    // Sweep direction (fast mode): with `alt`, odd segments sweep top-down,
+    // so the two rows a segment shares with each neighbour segment are loaded
+    // by both CTAs at about the same time (both at their start or both at
+    // their end) and the second load hits L2 instead of HBM.  A top-down
+    // sweep runs the SAME code on the mirror image y -> -y of the segment:
+    // rows are consumed in reverse order and hv enters negated; the scheme
+    // is mirror-symmetric and every IEEE operation is odd under negation, so
+    // the mirrored step yields exactly the negated hv' (and the same h', hu')
+    // -- up to the sign of zero results, which is why exact mode (bit-exact
+    // contract) always sweeps bottom-up.
+    const bool down = FAST && alt && (blockIdx.y & 1);
+    const int ytop = y0 + nrows;                         // top loaded row (halo above the segment)
+    auto stage_y = [&](int k) { return down ? ytop - k * R - (R - 1) : y0 - 1 + k * R; };
+    const float vsign = down ? -1.0f : 1.0f;
+    const int row_bytes = down ? -(G::LOAD * 4) : G::LOAD * 4;   // stage row step in the sweep order
     const uint32_t ring = sbase + warp * G::WARP_RING;
     const uint32_t full = sbase + WARPS * G::WARP_RING + warp * tma::S * 8;
 
@@ -208,7 +223,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int k = 0; k < tma::S - 1 && k < nstages; ++k)
-            issue_stage<CPL>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, y0 - 1 + k * R);
+            issue_stage<CPL>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, stage_y(k));
     }
     __syncwarp();
 
@@ -245,16 +260,22 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             const int kn = k + tma::S - 1;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_stage<CPL>(ring + (kn % tma::S) * G::STAGE_BYTES, full + 8 * (kn % tma::S), &tmH, &tmU, &tmV, tx,
-                             y0 - 1 + kn * R);
+                             stage_y(kn));
         }
         mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
-        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off;
+        // first row of the stage in sweep order (boxes are stored bottom-up)
+        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * (G::LOAD * 4) : 0);
 #pragma unroll UNR
         for (int r = 0; r < R; ++r) {
-            const int n = k * R + r;              // loaded row index; row y0-1+n
-            VecF<CPL> hv = lds_vec<CPL>(st + r * (G::LOAD * 4));
-            VecF<CPL> uv = lds_vec<CPL>(st + G::FIELD_BYTES + r * (G::LOAD * 4));
-            VecF<CPL> vv = lds_vec<CPL>(st + 2 * G::FIELD_BYTES + r * (G::LOAD * 4));
+            const int n = k * R + r;              // loaded row index; row y0-1+n (top-down: ytop-n)
+            const uint32_t sr = st + r * row_bytes;
+            VecF<CPL> hv = lds_vec<CPL>(sr);
+            VecF<CPL> uv = lds_vec<CPL>(sr + G::FIELD_BYTES);
+            VecF<CPL> vv = lds_vec<CPL>(sr + 2 * G::FIELD_BYTES);
+            if (FAST) {
+#pragma unroll
+                for (int i = 0; i < CPL; ++i) vv.v[i] *= vsign;   // mirror image (top-down sweep)
+            }
             if (any_bad) {
 #pragma unroll
                 for (int i = 0; i < CPL; ++i)
@@ -287,14 +308,18 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                     if (++fix_rows >= 16) fix_mode = false;
                 }
             }
-            // full-step update of the previous row (row y0 + n - 2)
+            // full-step update of the previous row (row y0 + n - 2; top-down: ytop - n + 1)
             if (n >= 2 && n <= nrows + 1) {
-                const int y = y0 + n - 2;
+                const int y = down ? ytop - n + 1 : y0 + n - 2;
                 float oh[CPL], ou[CPL], ov[CPL];
 #pragma unroll
                 for (int i = 0; i < CPL; ++i)
                     update_cell<float, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i],
                                            ydn[i], yup[i], c, oh[i], ou[i], ov[i]);
+                if (FAST) {
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) ov[i] *= vsign;   // back from the mirror image
+                }
                 if (owner) {
                     const int64_t off = (int64_t)y * pitch + X;
                     stg_vec<CPL>(oH + off, oh);
