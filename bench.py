@@ -139,7 +139,8 @@ def numpy_sample(n, rows):
 # device helpers
 # ---------------------------------------------------------------------------
 
-def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, boundary="reflective"):
+def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, boundary="reflective",
+                          precision="f32"):
     """Gaussian-hump initial state built on the device (setup only)."""
     import torch
     from paper_1107_2157_b200 import swdemo
@@ -147,14 +148,14 @@ def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, bound
     from paper_1107_2157_b200.region import Extent
     ng_x, ng_y = n_glob if n_glob else (n_x, n_y)
     full = Extent(n_x + 2, n_y + 2)
-    H, U, V = (DeviceField(full, "f32", device, fill=0.0) for _ in range(3))
+    H, U, V = (DeviceField(full, precision, device, fill=0.0) for _ in range(3))
     xs = (torch.arange(n_x, dtype=torch.float64, device=device) + x_off + 0.5) - ng_x / 2.0
     ys = (torch.arange(n_y, dtype=torch.float64, device=device) + y_off + 0.5) - ng_y / 2.0
     w = ng_x / 8.0
     for r0 in range(0, n_y, 2048):          # chunk to bound f64 temporaries
         r1 = min(n_y, r0 + 2048)
         h = 1.0 + 0.4 * torch.exp(-(xs[None, :] ** 2 + ys[r0:r1, None] ** 2) / (w * w))
-        H.data[1 + r0:1 + r1, 1:-1] = h.to(torch.float32)
+        H.data[1 + r0:1 + r1, 1:-1] = h.to(torch.float32 if precision == "f32" else torch.float64)
     st = swdemo.SWState(H, U, V)
     swdemo.apply_boundary(st, boundary)
     return st
@@ -171,6 +172,8 @@ def main():
                     help="fast: FMA + approximate reciprocals, rtol 2e-5 vs the oracle (headline); "
                          "exact: bit-identical to the oracle")
     ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
+                    help="field precision (f64: 48 B/cell; the headline is f32, BASELINE configs)")
     ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
     ap.add_argument("--alt", type=int, default=1, choices=[0, 1],
                     help="TMA kernel: odd segments sweep top-down (L2 reuse of shared halo rows)")
@@ -221,23 +224,24 @@ def main():
     if args.seg:
         N.check(N.lib().fkc_set_tma_segment(args.seg))
     N.check(N.lib().fkc_set_tma_alternate(args.alt))
-    st = device_gaussian_state(n, n, dev)
+    st = device_gaussian_state(n, n, dev, precision=args.precision)
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0
-    r = time_steps(st, n, dt, args.mode, args.variant, args.steps, args.warmup, sample_clocks=True)
+    r = time_steps(st, n, dt, args.mode, args.variant, args.steps, args.warmup, sample_clocks=True,
+                   precision=args.precision)
     total_ms, per_launch, clocks = r["total_ms"], r["per_launch"], r["clocks"]
     ms_step = total_ms / args.steps
     cells = n * n
     value = cells * args.steps / (total_ms / 1e3) / 1e9
     avg_launch_ms = sum(per_launch) / len(per_launch)
-    bytes_launch = BYTES_PER_CELL["f32"] * cells
+    bytes_launch = BYTES_PER_CELL[args.precision] * cells
     achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     other_line = None
     if not args.no_other:
         other = "exact" if args.mode == "fast" else "fast"
-        st2 = device_gaussian_state(n, n, dev)
-        r2 = time_steps(st2, n, dt, other, args.variant, min(args.steps, 20), 10)
+        st2 = device_gaussian_state(n, n, dev, precision=args.precision)
+        r2 = time_steps(st2, n, dt, other, args.variant, min(args.steps, 20), 10, precision=args.precision)
         del st2
         other_line = {"mode": other, "value": round(cells * r2["steps"] / (r2["total_ms"] / 1e3) / 1e9, 3),
                       "ms_per_step": round(r2["total_ms"] / r2["steps"], 5), "steps": r2["steps"],
@@ -248,7 +252,7 @@ def main():
     if os.path.exists(tp):
         try:
             t = json.load(open(tp))
-            key = f"{args.mode}_{n}"
+            key = f"{args.mode}_{n}" + ("" if args.precision == "f32" else "_f64")
             traffic = t.get(key)
         except Exception:
             traffic = None
@@ -256,13 +260,16 @@ def main():
     line = {
         "metric": "Gcell-updates/s (shallow-water step)", "value": round(value, 3), "unit": "Gcell-updates/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic (Gaussian hump h=1+0.4exp(-r^2/(n/8)^2), hu=hv=0)",
-        "config": {"workload": f"shallow-water {n}x{n} fp32, reflective, fixed dt=0.3*stable_dt (BASELINE config 3)",
+        "config": {"workload": f"shallow-water {n}x{n} {'fp32' if args.precision == 'f32' else 'fp64'}, reflective, "
+                               f"fixed dt=0.3*stable_dt (BASELINE config 3)",
+                   "precision": args.precision,
                    "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else
                    f"rtol {FAST_RTOL} vs oracle (tests/test_gpu_parity.py)",
                    "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",
-                   "l2": f"working set {6 * 4 * (n + 2) * (n + 2) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
+                   "l2": f"working set {BYTES_PER_CELL[args.precision] * (n + 2) * (n + 2) / 1e9:.1f} GB >> "
+                         "126 MB L2 (no flush needed)"},
         "hbm_gbs": round(achieved, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_source": peak_src, "traffic": traffic,
@@ -273,7 +280,7 @@ def main():
         "other_mode": other_line,
     }
 
-    if not args.no_e2e:
+    if not args.no_e2e and args.precision == "f32":
         line["e2e"] = e2e_run(n, dt, args, dev)
     if not args.no_cpu:
         try:
@@ -286,12 +293,13 @@ def main():
     return 0
 
 
-def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False):
+def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32"):
     """K steps of the fused step kernel, CUDA events on the launching stream
     (one event pair per launch: the step kernel is the only launch)."""
     import torch
     from paper_1107_2157_b200 import swdemo
-    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps + warmup, dt=dt, mode=mode, variant=variant)
+    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps + warmup, dt=dt, mode=mode, variant=variant,
+                          precision=precision)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)

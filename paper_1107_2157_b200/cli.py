@@ -8,7 +8,8 @@ the solver path, executed by the B200 engine:
 * ``run``     (cmd_run): config file -> diagnostics CSV and
   final-state CSVs in DIR; prints wall-clock total and per-step mean.
 * ``compare`` (cmd_compare): elementwise relative
-  difference of two run directories; prints the worst offender.
+  difference of two run directories (denominator floored at 1e-3 of the
+  field's scale); prints the worst offender.
 * ``bench``   (cmd_bench): per-step mean time per engine
   and interior width, CSV on stdout; asserts nothing.
 
@@ -100,12 +101,21 @@ def cmd_run(args) -> int:
     return EXIT_OK
 
 
+FLOOR = 1e-3   # denominators are floored at FLOOR x the field's max |value|
+
+
 def _rel_worst(a: np.ndarray, b: np.ndarray):
-    """max over cells of |a-b| / max(|a|,|b|) (0 where both are 0; inf where
-    exactly one is non-finite) and the argmax (row, col)."""
+    """max over cells of |a-b| / max(|a|, |b|, FLOOR * scale), scale = the
+    larger max |value| of the two fields (0 where a == b; inf where exactly
+    one is non-finite), and the argmax (row, col).  The floor keeps values
+    far below the field's scale -- a momentum of 1e-10 next to 0 in a field
+    of magnitude 0.05 -- from counting as 100 % differences, which is what
+    lets f32 and f64 runs compare at rtol 1e-4."""
     a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    fin = np.isfinite(a64) & np.isfinite(b64)
+    scale = max(float(np.max(np.abs(a64[fin]), initial=0.0)), float(np.max(np.abs(b64[fin]), initial=0.0)))
     with np.errstate(invalid="ignore", divide="ignore"):
-        den = np.maximum(np.abs(a64), np.abs(b64))
+        den = np.maximum(np.maximum(np.abs(a64), np.abs(b64)), FLOOR * scale)
         rel = np.where(a64 == b64, 0.0, np.abs(a64 - b64) / den)
     rel = np.where(np.isnan(rel), np.inf, rel)
     idx = np.unravel_index(int(np.argmax(rel)), rel.shape) if rel.size else (0, 0)

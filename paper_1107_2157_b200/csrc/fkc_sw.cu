@@ -104,10 +104,10 @@ int valid_peers(const fkc_sw_step_args* a) {
     return FKC_OK;
 }
 
-bool peers_tma_ok(const fkc_sw_step_args* a) {
+bool peers_tma_ok(const fkc_sw_step_args* a, int es) {
     for (int s = 2; s < 4; ++s)
         for (int f = 0; f < 3; ++f)
-            if (a->peer[s].p[0] && (((uintptr_t)a->peer[s].p[f]) + 4) % 16 != 0) return false;
+            if (a->peer[s].p[0] && (((uintptr_t)a->peer[s].p[f]) + es) % 16 != 0) return false;
     return true;
 }
 
@@ -136,9 +136,10 @@ struct MapKey {
     const void* p;
     int nx, ny;
     int64_t pitch;
-    int boxw, boxh;
+    int boxw, boxh, esize;
     bool operator==(const MapKey& o) const {
-        return p == o.p && nx == o.nx && ny == o.ny && pitch == o.pitch && boxw == o.boxw && boxh == o.boxh;
+        return p == o.p && nx == o.nx && ny == o.ny && pitch == o.pitch && boxw == o.boxw && boxh == o.boxh &&
+               esize == o.esize;
     }
 };
 
@@ -151,21 +152,24 @@ struct MapCache {
 };
 MapCache g_maps;
 
-// Map over one f32 field whose element (0,0) is at `p`: tensor column t is
-// full column t-3, so box starts stay 16-B aligned when column 1 is.
-int get_map(const void* p, int nx, int ny, int64_t pitch, int boxw, CUtensorMap* out) {
-    MapKey k{p, nx, ny, pitch, boxw, tma::R};
+// Map over one field (f32 / f64, element size esize) whose element (0,0) is
+// at `p`: tensor column t is full column t - (CPL-1), CPL = 16 / esize, so
+// box starts stay 16-B aligned when column 1 is.
+int get_map(const void* p, int nx, int ny, int64_t pitch, int boxw, int esize, CUtensorMap* out) {
+    MapKey k{p, nx, ny, pitch, boxw, tma::R, esize};
     std::lock_guard<std::mutex> lk(g_maps.mu);
     for (int i = 0; i < g_maps.used; ++i)
         if (g_maps.key[i] == k) { *out = g_maps.map[i]; return FKC_OK; }
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(FKC_ECUDA, "cuTensorMapEncodeTiled unavailable");
     alignas(64) CUtensorMap m;
-    cuuint64_t dims[2] = {(cuuint64_t)nx + 5, (cuuint64_t)ny + 2};
-    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    const int lead = 16 / esize - 1;
+    cuuint64_t dims[2] = {(cuuint64_t)nx + 2 + lead, (cuuint64_t)ny + 2};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * esize};
     cuuint32_t box[2] = {(cuuint32_t)boxw, (cuuint32_t)tma::R};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)((const float*)p - 3), dims, strides, box, estr,
+    CUresult r = fn(&m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                    (void*)((const char*)p - (size_t)lead * esize), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FKC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -180,11 +184,12 @@ int get_map(const void* p, int nx, int ny, int64_t pitch, int boxw, CUtensorMap*
 
 bool tma_eligible(const fkc_sw_step_args* a) {
     const fkc_grid& g = a->grid;
-    if (g.dtype != FKC_F32 || (g.nx % 4) != 0 || (g.pitch % 4) != 0) return false;
+    const int es = g.dtype == FKC_F32 ? 4 : 8, cpl = 16 / es;
+    if ((g.nx % cpl) != 0 || (g.pitch % cpl) != 0) return false;
     const void* ps[6] = {a->H, a->U, a->V, a->oH, a->oU, a->oV};
     for (const void* p : ps)
-        if ((((uintptr_t)p) + 4) % 16 != 0) return false;
-    return peers_tma_ok(a);
+        if ((((uintptr_t)p) + es) % 16 != 0) return false;
+    return peers_tma_ok(a, es);
 }
 
 template <class T>
@@ -225,11 +230,11 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     return seg;
 }
 
-template <int CPL, bool FAST, bool RED>
+template <class T, bool FAST, bool RED>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
-    using G = tma::Geo<CPL>;
+    using G = tma::Geo<T>;
     static bool attr_set = false;
-    auto kern = sw_step_tma<CPL, FAST, RED>;
+    auto kern = sw_step_tma<T, FAST, RED>;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
         attr_set = true;
@@ -240,28 +245,29 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const int seg = pick_seg(nbands, g.ny, G::template ctas_per_sm<FAST>());
     dim3 grd(nbands, (g.ny + seg - 1) / seg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, g_alt, (float*)a->oH,
-                                                   (float*)a->oU, (float*)a->oV, (float)a->dx, (float)a->dy,
-                                                   dts, (float)a->g, to_bcs(a->bc), to_red(a->red),
-                                                   to_peers(a), to_sync(a));
+    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, g_alt, (T*)a->oH,
+                                                   (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
+                                                   to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
 }
 
-template <int CPL>
-int launch_tma_cpl(const fkc_sw_step_args* a, cudaStream_t st) {
+template <class T>
+int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
     CUtensorMap m[3];  // H, U, V
     const fkc_grid& g = a->grid;
     const void* ps[3] = {a->H, a->U, a->V};
     int rc;
     for (int f = 0; f < 3; ++f)
-        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<CPL>::LOAD, &m[f]))) return rc;
+        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<T>::LOAD, (int)sizeof(T), &m[f]))) return rc;
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(to_red(a->red));
-    if (fast) return r ? launch_tma_t<CPL, true, true>(a, st, m) : launch_tma_t<CPL, true, false>(a, st, m);
-    return r ? launch_tma_t<CPL, false, true>(a, st, m) : launch_tma_t<CPL, false, false>(a, st, m);
+    if (fast) return r ? launch_tma_t<T, true, true>(a, st, m) : launch_tma_t<T, true, false>(a, st, m);
+    return r ? launch_tma_t<T, false, true>(a, st, m) : launch_tma_t<T, false, false>(a, st, m);
 }
 
-int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) { return launch_tma_cpl<4>(a, st); }
+int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
+    return a->grid.dtype == FKC_F32 ? launch_tma_typed<float>(a, st) : launch_tma_typed<double>(a, st);
+}
 
 }  // namespace
 
@@ -310,8 +316,8 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (variant == FKC_VARIANT_AUTO) variant = tma_eligible(a) ? FKC_VARIANT_TMA : FKC_VARIANT_GENERIC;
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
-            return fail(FKC_EUSAGE, "TMA variant needs f32, nx%%4==0, pitch%%4==0 and (ptr+1) 16-B aligned "
-                                    "(fields and row peer lines)");
+            return fail(FKC_EUSAGE, "TMA variant needs nx and pitch multiples of 16/elem_size and (ptr+1 elem) "
+                                    "16-B aligned (fields and row peer lines)");
         return launch_tma(a, st);
     }
     if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");

@@ -38,14 +38,19 @@ constexpr int WARPS = 4;                 // warps (strips) per CTA
 #endif
 constexpr int R = FKC_TMA_R;             // rows per stage
 constexpr int S = FKC_TMA_S;             // ring stages per warp
-template <int CPL> struct Geo {
+// T = float (4 cells per lane) or double (2 cells per lane): one 16-byte
+// vector per lane and row either way.
+template <class T> struct Geo {
+    static constexpr int CPL = 16 / (int)sizeof(T);       // cells per lane
     static constexpr int LOAD = 32 * CPL;                 // columns loaded per strip
     static constexpr int OWN = 30 * CPL;                  // columns owned per strip
-    static constexpr int FIELD_BYTES = R * LOAD * 4;
+    static constexpr int FIELD_BYTES = R * LOAD * (int)sizeof(T);
     static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
     static constexpr int WARP_RING = S * STAGE_BYTES;
     static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
-    template <bool FAST> static constexpr int ctas_per_sm() { return FAST ? FKC_TMA_CTAS_FAST : FKC_TMA_CTAS_EXACT; }
+    template <bool FAST> static constexpr int ctas_per_sm() {
+        return sizeof(T) == 8 ? 2 : (FAST ? FKC_TMA_CTAS_FAST : FKC_TMA_CTAS_EXACT);
+    }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
 constexpr int THREADS = WARPS * 32;
@@ -97,34 +102,35 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         :: "r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar) : "memory");
 }
 
-// CPL consecutive floats: shared-memory load, global store.
-template <int CPL> struct VecF {
-    float v[CPL];
+// One lane's 16-byte vector of a row (4 floats or 2 doubles): shared-memory
+// load, global store.
+template <class T> struct VecF {
+    T v[16 / sizeof(T)];
 };
-template <int CPL>
-__device__ __forceinline__ VecF<CPL> lds_vec(uint32_t a) {
-    VecF<CPL> r;
-    if constexpr (CPL == 4)
+template <class T>
+__device__ __forceinline__ VecF<T> lds_vec(uint32_t a) {
+    VecF<T> r;
+    if constexpr (sizeof(T) == 4)
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(a));
     else
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.v[0]), "=f"(r.v[1]) : "r"(a));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "r"(a));
     return r;
 }
-template <int CPL>
-__device__ __forceinline__ void stg_vec(float* p, const float (&v)[CPL], float sgn = 1.0f) {
-    if constexpr (CPL == 4)
+template <class T, int CPL>
+__device__ __forceinline__ void stg_vec(T* p, const T (&v)[CPL], T sgn = T(1)) {
+    if constexpr (sizeof(T) == 4)
         *(float4*)p = make_float4(sgn * v[0], sgn * v[1], sgn * v[2], sgn * v[3]);
     else
-        *(float2*)p = make_float2(sgn * v[0], sgn * v[1]);
+        *(double2*)p = make_double2(sgn * v[0], sgn * v[1]);
 }
 
 // One stage = R rows x LOAD columns of H, U, V (3 boxes), completing on `bar`.
-template <int CPL>
+template <class T>
 __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUtensorMap* mH,
                                             const CUtensorMap* mU, const CUtensorMap* mV, int tx, int ty) {
-    constexpr int FB = tma::Geo<CPL>::FIELD_BYTES;
-    mbar_expect_tx(bar, tma::Geo<CPL>::STAGE_BYTES);
+    constexpr int FB = tma::Geo<T>::FIELD_BYTES;
+    mbar_expect_tx(bar, tma::Geo<T>::STAGE_BYTES);
     tma_load_2d(st, mH, tx, ty, bar);
     tma_load_2d(st + FB, mU, tx, ty, bar);
     tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
@@ -134,50 +140,51 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
 // the previous row pc and this row (if have_prev), and the x-faces of this
 // row (if want_x): nxr[i] = face between cell i and i+1 of the lane (cell
 // CPL comes from lane+1), nxl = face left of cell 0 (= nxr[CPL-1] of lane-1).
-template <int DM, int CPL>
-__device__ __forceinline__ void row_faces(const VecF<CPL>& h, const VecF<CPL>& u, const VecF<CPL>& v,
-                                          const CellQ<float> (&pc)[CPL], bool have_prev, bool want_x,
-                                          const Coef<float>& c, CellQ<float> (&nc)[CPL],
-                                          FaceF<float> (&yup)[CPL], FaceF<float> (&nxr)[CPL],
-                                          FaceF<float>& nxl, bool& ok) {
+template <class T, int DM, int CPL>
+__device__ __forceinline__ void row_faces(const VecF<T>& h, const VecF<T>& u, const VecF<T>& v,
+                                          const CellQ<T> (&pc)[CPL], bool have_prev, bool want_x,
+                                          const Coef<T>& c, CellQ<T> (&nc)[CPL],
+                                          FaceF<T> (&yup)[CPL], FaceF<T> (&nxr)[CPL],
+                                          FaceF<T>& nxl, bool& ok) {
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) nc[i] = cell_q<float, DM>(h.v[i], u.v[i], v.v[i], c, ok);
+    for (int i = 0; i < CPL; ++i) nc[i] = cell_q<T, DM>(h.v[i], u.v[i], v.v[i], c, ok);
     if (have_prev) {
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) yup[i] = y_face<float, DM>(pc[i], nc[i], c, ok);
+        for (int i = 0; i < CPL; ++i) yup[i] = y_face<T, DM>(pc[i], nc[i], c, ok);
     }
     if (want_x) {
-        CellQ<float> nb;  // first cell of lane+1
+        CellQ<T> nb;  // first cell of lane+1
         nb.h = __shfl_down_sync(0xffffffffu, nc[0].h, 1);
         nb.u = __shfl_down_sync(0xffffffffu, nc[0].u, 1);
         nb.v = __shfl_down_sync(0xffffffffu, nc[0].v, 1);
         nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu, 1);
         nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr, 1);
-        nb.fv = 0.f;
+        nb.fv = T(0);
 #pragma unroll
-        for (int i = 0; i < CPL - 1; ++i) nxr[i] = x_face<float, DM>(nc[i], nc[i + 1], c, ok);
-        nxr[CPL - 1] = x_face<float, DM>(nc[CPL - 1], nb, c, ok);
+        for (int i = 0; i < CPL - 1; ++i) nxr[i] = x_face<T, DM>(nc[i], nc[i + 1], c, ok);
+        nxr[CPL - 1] = x_face<T, DM>(nc[CPL - 1], nb, c, ok);
         nxl.fh = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fh, 1);
         nxl.fu = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fu, 1);
         nxl.fv = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fv, 1);
     }
 }
 
-// Tensor coordinates: the maps are encoded with base = &field(-3, 0) so that
-// full-array column x is tensor column x + 3 (16-B aligned boxes).  Strip j
-// owns columns [1 + OWN j, OWN (j+1)] and loads full columns
-// [1 + OWN j - CPL, OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
-template <int CPL, bool FAST, bool RED>
-__global__ void __launch_bounds__(tma::THREADS, tma::Geo<CPL>::template ctas_per_sm<FAST>())
+// Tensor coordinates: the maps are encoded with base = &field(1 - CPL, 0)
+// so that full-array column x is tensor column x + CPL - 1 (16-B aligned
+// boxes: cell 1 is 128-B aligned).  Strip j owns columns
+// [1 + OWN j, OWN (j+1)] and loads full columns [1 + OWN j - CPL,
+// OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
+template <class T, bool FAST, bool RED>
+__global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg, int alt,
-            float* __restrict__ oH, float* __restrict__ oU, float* __restrict__ oV,
-            float dx, float dy, DtSrc dts, float g, BCs bc, RedPtrs red, Peers P, SyncArgs sy) {
+            T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
+            T dx, T dy, DtSrc dts, T g, BCs bc, RedPtrs red, Peers P, SyncArgs sy) {
     using namespace tma;
-    using G = Geo<CPL>;
-    // CPL = 4 keeps every TMA box start (tensor column 120 j) 16-byte aligned;
-    // narrower lanes would need wider ghost margins to stay aligned.
-    static_assert(CPL == 4, "the strip geometry assumes 4 cells (one float4) per lane");
+    using G = Geo<T>;
+    constexpr int CPL = G::CPL;
+    // one 16-byte vector per lane keeps every TMA box start (tensor column
+    // OWN j, i.e. 480 j bytes) 16-byte aligned
     constexpr int DM = FAST ? DIV_FAST : DIV_GUARD;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
@@ -186,7 +193,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * WARPS + warp;
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
-    const int tx = xs + 3;                               // its tensor column
+    const int tx = xs + CPL - 1;                         // its tensor column
     if (xs + CPL > nx) return;                           // strip owns nothing (ragged last band)
     const int y0 = 1 + blockIdx.y * seg;                 // first interior row of the segment
     const int nrows = min(seg, ny - y0 + 1);
@@ -205,8 +212,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const bool down = FAST && alt && (blockIdx.y & 1);
     const int ytop = y0 + nrows;                         // top loaded row (halo above the segment)
     auto stage_y = [&](int k) { return down ? ytop - k * R - (R - 1) : y0 - 1 + k * R; };
-    const float vsign = down ? -1.0f : 1.0f;
-    const int row_bytes = down ? -(G::LOAD * 4) : G::LOAD * 4;   // stage row step in the sweep order
+    const T vsign = down ? T(-1) : T(1);
+    const int row_bytes = down ? -(G::LOAD * (int)sizeof(T)) : G::LOAD * (int)sizeof(T);   // stage row step
     const uint32_t ring = sbase + warp * G::WARP_RING;
     const uint32_t full = sbase + WARPS * G::WARP_RING + warp * tma::S * 8;
 
@@ -223,13 +230,13 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int k = 0; k < tma::S - 1 && k < nstages; ++k)
-            issue_stage<CPL>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, stage_y(k));
+            issue_stage<T>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, stage_y(k));
     }
     __syncwarp();
 
-    const float dt = resolve_dt<float>(dts);
-    const Coef<float> c = make_coef<float>(dx, dy, dt, g);
-    const float dmin = dx < dy ? dx : dy;
+    const T dt = resolve_dt<T>(dts);
+    const Coef<T> c = make_coef<T>(dx, dy, dt, g);
+    const T dmin = dx < dy ? dx : dy;
     const int X = xs + CPL * lane;             // full column of cell 0 of this lane
     const bool owner = (lane >= 1) && (lane <= 30) && (X <= nx);   // nx % CPL == 0
     // cells whose loaded data is not part of the grid (padding left of column
@@ -242,12 +249,12 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const bool any_bad = __any_sync(0xffffffffu, bad != 0);
     const bool edge_rows = (y0 == 1) || (y0 + nrows - 1 == ny);
     const bool edge_cols = owner && ((X == 1) || (X + CPL - 1 == nx));
-    const uint32_t lane_off = 4u * CPL * lane;
+    const uint32_t lane_off = 16u * lane;
 
-    CellQ<float> pc[CPL];              // previous row's cells
-    FaceF<float> pxl, pxr[CPL];        // previous row's x-face fluxes
-    FaceF<float> ydn[CPL];             // y-face below the previous row
-    RedAcc<float> acc;
+    CellQ<T> pc[CPL];                  // previous row's cells
+    FaceF<T> pxl, pxr[CPL];            // previous row's x-face fluxes
+    FaceF<T> ydn[CPL];                 // y-face below the previous row
+    RedAcc<T> acc;
     acc.init();
     bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
     int fix_rows = 0;
@@ -259,19 +266,19 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         if (lane == 0 && k + tma::S - 1 < nstages) {
             const int kn = k + tma::S - 1;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_stage<CPL>(ring + (kn % tma::S) * G::STAGE_BYTES, full + 8 * (kn % tma::S), &tmH, &tmU, &tmV, tx,
+            issue_stage<T>(ring + (kn % tma::S) * G::STAGE_BYTES, full + 8 * (kn % tma::S), &tmH, &tmU, &tmV, tx,
                              stage_y(kn));
         }
         mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
         // first row of the stage in sweep order (boxes are stored bottom-up)
-        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * (G::LOAD * 4) : 0);
+        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * (G::LOAD * (int)sizeof(T)) : 0);
 #pragma unroll UNR
         for (int r = 0; r < R; ++r) {
             const int n = k * R + r;              // loaded row index; row y0-1+n (top-down: ytop-n)
             const uint32_t sr = st + r * row_bytes;
-            VecF<CPL> hv = lds_vec<CPL>(sr);
-            VecF<CPL> uv = lds_vec<CPL>(sr + G::FIELD_BYTES);
-            VecF<CPL> vv = lds_vec<CPL>(sr + 2 * G::FIELD_BYTES);
+            VecF<T> hv = lds_vec<T>(sr);
+            VecF<T> uv = lds_vec<T>(sr + G::FIELD_BYTES);
+            VecF<T> vv = lds_vec<T>(sr + 2 * G::FIELD_BYTES);
             if (FAST) {
 #pragma unroll
                 for (int i = 0; i < CPL; ++i) vv.v[i] *= vsign;   // mirror image (top-down sweep)
@@ -279,15 +286,15 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             if (any_bad) {
 #pragma unroll
                 for (int i = 0; i < CPL; ++i)
-                    if (bad & (1 << i)) { hv.v[i] = 1.f; uv.v[i] = 0.f; vv.v[i] = 0.f; }
+                    if (bad & (1 << i)) { hv.v[i] = T(1); uv.v[i] = T(0); vv.v[i] = T(0); }
             }
             const bool have_prev = n >= 1;
             const bool want_x = (n >= 1) && (n <= nrows);
-            CellQ<float> nc[CPL];
-            FaceF<float> yup[CPL], nxl, nxr[CPL];
+            CellQ<T> nc[CPL];
+            FaceF<T> yup[CPL], nxl, nxr[CPL];
             bool ok = true;
             if (FAST) {
-                row_faces<DIV_FAST, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                row_faces<T, DIV_FAST, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
             } else {
                 // exact mode, warp-uniform per row: lean guarded division;
                 // if any lane saw a non-benign operand, redo the row with the
@@ -297,24 +304,24 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 // fixup variant the next rows start with it and the lean
                 // variant is retried every 16 rows.
                 if (!fix_mode && !FKC_EXACT_ALWAYS_FIXUP) {
-                    row_faces<DIV_GUARD, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    row_faces<T, DIV_GUARD, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
                     if (__any_sync(0xffffffffu, !ok)) {
                         fix_mode = true;
                         fix_rows = 0;
-                        row_faces<DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                        row_faces<T, DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
                     }
                 } else {
-                    row_faces<DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    row_faces<T, DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
                     if (++fix_rows >= 16) fix_mode = false;
                 }
             }
             // full-step update of the previous row (row y0 + n - 2; top-down: ytop - n + 1)
             if (n >= 2 && n <= nrows + 1) {
                 const int y = down ? ytop - n + 1 : y0 + n - 2;
-                float oh[CPL], ou[CPL], ov[CPL];
+                T oh[CPL], ou[CPL], ov[CPL];
 #pragma unroll
                 for (int i = 0; i < CPL; ++i)
-                    update_cell<float, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i],
+                    update_cell<T, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i],
                                            ydn[i], yup[i], c, oh[i], ou[i], ov[i]);
                 if (FAST) {
 #pragma unroll
@@ -322,49 +329,49 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 }
                 if (owner) {
                     const int64_t off = (int64_t)y * pitch + X;
-                    stg_vec<CPL>(oH + off, oh);
-                    stg_vec<CPL>(oU + off, ou);
-                    stg_vec<CPL>(oV + off, ov);
+                    stg_vec<T, CPL>(oH + off, oh);
+                    stg_vec<T, CPL>(oU + off, ou);
+                    stg_vec<T, CPL>(oV + off, ov);
                     // fused boundary fill of the output halo
                     if (edge_rows && (y == 1 || y == ny)) {
                         const bool refl = (y == 1 && bc.s[SIDE_D] == BC_REFL) || (y == ny && bc.s[SIDE_U] == BC_REFL);
                         const bool per = (y == 1 && bc.s[SIDE_U] == BC_PER) || (y == ny && bc.s[SIDE_D] == BC_PER);
                         if (refl) {
                             const int64_t o2 = (int64_t)(y == 1 ? 0 : ny + 1) * pitch + X;
-                            stg_vec<CPL>(oH + o2, oh);
-                            stg_vec<CPL>(oU + o2, ou);
-                            stg_vec<CPL>(oV + o2, ov, -1.0f);
+                            stg_vec<T, CPL>(oH + o2, oh);
+                            stg_vec<T, CPL>(oU + o2, ou);
+                            stg_vec<T, CPL>(oV + o2, ov, T(-1));
                         }
                         if (per) {
                             const int64_t o2 = (int64_t)(y == 1 ? ny + 1 : 0) * pitch + X;
-                            stg_vec<CPL>(oH + o2, oh);
-                            stg_vec<CPL>(oU + o2, ou);
-                            stg_vec<CPL>(oV + o2, ov);
+                            stg_vec<T, CPL>(oH + o2, oh);
+                            stg_vec<T, CPL>(oU + o2, ou);
+                            stg_vec<T, CPL>(oV + o2, ov);
                         }
                         // fused halo exchange: the new row goes straight into
                         // the neighbour tile's halo row (rows: stride 1)
                         const PeerLine& pl = P.s[y == 1 ? SIDE_D : SIDE_U];
                         if (pl.p[0]) {
-                            stg_vec<CPL>((float*)pl.p[0] + X, oh);
-                            stg_vec<CPL>((float*)pl.p[1] + X, ou);
-                            stg_vec<CPL>((float*)pl.p[2] + X, ov);
+                            stg_vec<T, CPL>((T*)pl.p[0] + X, oh);
+                            stg_vec<T, CPL>((T*)pl.p[1] + X, ou);
+                            stg_vec<T, CPL>((T*)pl.p[2] + X, ov);
                         }
                         if (y == 1 && y == ny && P.s[SIDE_U].p[0]) {   // single-row tile
-                            stg_vec<CPL>((float*)P.s[SIDE_U].p[0] + X, oh);
-                            stg_vec<CPL>((float*)P.s[SIDE_U].p[1] + X, ou);
-                            stg_vec<CPL>((float*)P.s[SIDE_U].p[2] + X, ov);
+                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[0] + X, oh);
+                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[1] + X, ou);
+                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[2] + X, ov);
                         }
                     }
                     if (edge_cols) {
                         if (X == 1) {
-                            emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, 1, y, oh[0], ou[0], ov[0], false);
-                            if (P.s[SIDE_L].p[0]) peer_store<float>(P.s[SIDE_L], y, oh[0], ou[0], ov[0]);
+                            emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, 1, y, oh[0], ou[0], ov[0], false);
+                            if (P.s[SIDE_L].p[0]) peer_store<T>(P.s[SIDE_L], y, oh[0], ou[0], ov[0]);
                         }
                         if (X + CPL - 1 == nx) {
-                            emit_halos<float>(oH, oU, oV, pitch, nx, ny, bc, nx, y, oh[CPL - 1], ou[CPL - 1],
-                                              ov[CPL - 1], false);
+                            emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, nx, y, oh[CPL - 1], ou[CPL - 1],
+                                          ov[CPL - 1], false);
                             if (P.s[SIDE_R].p[0])
-                                peer_store<float>(P.s[SIDE_R], y, oh[CPL - 1], ou[CPL - 1], ov[CPL - 1]);
+                                peer_store<T>(P.s[SIDE_R], y, oh[CPL - 1], ou[CPL - 1], ov[CPL - 1]);
                         }
                     }
                     if (RED) {
@@ -392,7 +399,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         const int expected[4] = {(int)gridDim.y, (int)gridDim.y, nstrips, nstrips};
         if (lane == 0) peer_signal(sy, sides, expected);
     }
-    if (RED) warp_reduce_commit<float>(acc, red, lane);
+    if (RED) warp_reduce_commit<T>(acc, red, lane);
 }
 
 }  // namespace fkc
