@@ -7,9 +7,10 @@ the solver path, executed by the B200 engine:
 
 * ``run``     (cmd_run): config file -> diagnostics CSV and
   final-state CSVs in DIR; prints wall-clock total and per-step mean.
-* ``compare`` (cmd_compare): elementwise relative
-  difference of two run directories (denominator floored at 1e-3 of the
-  field's scale); prints the worst offender.
+* ``compare`` (cmd_compare): relative difference of two
+  run directories, per cell against max(|a|, |b|, floor x field scale)
+  (``--floor``: 1 = normwise, 0 = strictly elementwise); prints the worst
+  offender.
 * ``bench``   (cmd_bench): per-step mean time per engine
   and interior width, CSV on stdout; asserts nothing.
 
@@ -55,6 +56,9 @@ def _parser() -> argparse.ArgumentParser:
     c.add_argument("a")
     c.add_argument("b")
     c.add_argument("--rtol", type=float, default=0.0)
+    c.add_argument("--floor", type=float, default=1.0,
+                   help="relative-difference denominator floor, as a fraction of the field's max |value| "
+                        "(1: normwise, 0: strictly elementwise)")
     b = sub.add_parser("bench", help="per-step time per engine and width (CSV)")
     b.add_argument("config")
     b.add_argument("--sizes", default="16,32,64,128,256,512,1024,2048,4096")
@@ -101,21 +105,19 @@ def cmd_run(args) -> int:
     return EXIT_OK
 
 
-FLOOR = 1e-3   # denominators are floored at FLOOR x the field's max |value|
-
-
-def _rel_worst(a: np.ndarray, b: np.ndarray):
-    """max over cells of |a-b| / max(|a|, |b|, FLOOR * scale), scale = the
+def _rel_worst(a: np.ndarray, b: np.ndarray, floor: float = 1.0):
+    """max over cells of |a-b| / max(|a|, |b|, floor * scale), scale = the
     larger max |value| of the two fields (0 where a == b; inf where exactly
-    one is non-finite), and the argmax (row, col).  The floor keeps values
-    far below the field's scale -- a momentum of 1e-10 next to 0 in a field
-    of magnitude 0.05 -- from counting as 100 % differences, which is what
-    lets f32 and f64 runs compare at rtol 1e-4."""
+    one is non-finite), and the argmax (row, col).  floor = 1 (default) is
+    the normwise relative difference, |a-b| / max|field|: round-off of the
+    O(g h^2) fluxes leaves absolute errors of ~1e-6 on small f32 momenta,
+    which is what lets f32 and f64 runs compare at rtol 1e-4 (SPEC.md:618);
+    floor = 0 is the strict elementwise relative difference."""
     a64, b64 = a.astype(np.float64), b.astype(np.float64)
     fin = np.isfinite(a64) & np.isfinite(b64)
     scale = max(float(np.max(np.abs(a64[fin]), initial=0.0)), float(np.max(np.abs(b64[fin]), initial=0.0)))
     with np.errstate(invalid="ignore", divide="ignore"):
-        den = np.maximum(np.maximum(np.abs(a64), np.abs(b64)), FLOOR * scale)
+        den = np.maximum(np.maximum(np.abs(a64), np.abs(b64)), floor * scale)
         rel = np.where(a64 == b64, 0.0, np.abs(a64 - b64) / den)
     rel = np.where(np.isnan(rel), np.inf, rel)
     idx = np.unravel_index(int(np.argmax(rel)), rel.shape) if rel.size else (0, 0)
@@ -133,7 +135,7 @@ def cmd_compare(args) -> int:
             if fa.data.shape != fb.data.shape:
                 print(f"fkc: shape mismatch in {name}: {fa.data.shape} vs {fb.data.shape}", file=sys.stderr)
                 return EXIT_USAGE
-            r, (y, x) = _rel_worst(fa.data, fb.data)
+            r, (y, x) = _rel_worst(fa.data, fb.data, args.floor)
             if r > worst[0] or worst[1] is None:
                 worst = (r, name, (int(x), int(y)), float(fa.data[y, x]), float(fb.data[y, x]))
         if os.path.exists(pa["diag"]) and os.path.exists(pb["diag"]):
@@ -142,7 +144,7 @@ def cmd_compare(args) -> int:
                 print(f"fkc: shape mismatch in diagnostics: {da.shape} vs {db.shape}", file=sys.stderr)
                 return EXIT_USAGE
             if da.size:
-                r, (row, col) = _rel_worst(da, db)
+                r, (row, col) = _rel_worst(da, db, args.floor)
                 if r > worst[0]:
                     worst = (r, "diagnostics", (int(col), int(row)), float(da[row, col]), float(db[row, col]))
     except (OSError, fieldio.FieldFormatError) as e:

@@ -77,6 +77,16 @@ def test_compare_exit_codes(tmp_path, capsys):
     out = capsys.readouterr().out
     assert "in H at (x, y) = (7, 5)" in out
     assert cli.main(["compare", a, c, "--rtol", "1e-2"]) == 0
+    assert cli.main(["compare", a, c, "--rtol", "1e-6", "--floor", "0"]) == 1
+    # a tiny value next to 0: 100 % elementwise, negligible normwise
+    U1 = U.copy()
+    U1[4, 4] = 1e-12
+    U2 = U.copy()
+    U2[4, 4] = 0.0
+    _write_run(a, H, U1, V, "f64", diag)
+    _write_run(c, H, U2, V, "f64", diag)
+    assert cli.main(["compare", a, c, "--rtol", "1e-6"]) == 0
+    assert cli.main(["compare", a, c, "--rtol", "1e-6", "--floor", "0"]) == 1
     d = str(tmp_path / "d")
     Hs, Us, Vs = so.random_state(20, 16, "f64", seed=9)
     _write_run(d, Hs, Us, Vs, "f64")
