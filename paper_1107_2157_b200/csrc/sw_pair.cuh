@@ -1,0 +1,188 @@
+// sw_pair.cuh -- row engines of the TMA kernel.
+//
+// An engine holds the register window of the y-sweep (the previous row's
+// cell quantities, its x-face fluxes, the y-face below it) and offers
+//   row<DM>(h, u, v, have_prev, want_x, c, ok)  -- faces of a freshly loaded row
+//   update<DM>(c, oh, ou, ov)                    -- full step of the previous row
+//   shift()                                      -- the new row becomes the previous one
+//
+// ScalarEngine: one scalar op per cell (any T; exact mode's bit-exact order).
+// PairEngine  : f32 fast mode on sm_100a's packed FP32 pipe.  A lane's four
+//   cells c0..c3 form the register pairs P0 = (c0, c1), P1 = (c2, c3) (as
+//   ld.shared.v4 delivers them) and every cell-wise or column-aligned
+//   operation -- the cell quantities, the y-faces between two rows, the
+//   full-step update -- is one FADD2 / FMUL2 / FFMA2 per pair, i.e. half the
+//   issue slots.  The x-faces pair cells that straddle the pairs (c1|c2,
+//   c3|lane+1), so they stay scalar and are stored directly as the per-cell
+//   differences F_left - F_right the update consumes.
+#pragma once
+#include "sw_kernels.cuh"
+
+namespace fkc {
+
+// one lane's 16-byte vector of a row: 4 floats or 2 doubles
+template <class T> struct VecF {
+    T v[16 / sizeof(T)];
+};
+
+template <class T, int CPL> struct ScalarEngine {
+    CellQ<T> pc[CPL];                  // previous row's cells
+    FaceF<T> pxl, pxr[CPL];            // previous row's x-face fluxes
+    FaceF<T> ydn[CPL];                 // y-face below the previous row
+    CellQ<T> nc[CPL];                  // new row
+    FaceF<T> yup[CPL], nxl, nxr[CPL];
+
+    template <int DM>
+    __device__ __forceinline__ void row(const VecF<T>& h, const VecF<T>& u, const VecF<T>& v, bool have_prev,
+                                        bool want_x, const Coef<T>& c, bool& ok) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) nc[i] = cell_q<T, DM>(h.v[i], u.v[i], v.v[i], c, ok);
+        if (have_prev) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) yup[i] = y_face<T, DM>(pc[i], nc[i], c, ok);
+        }
+        if (want_x) {
+            CellQ<T> nb;  // first cell of lane+1
+            nb.h = __shfl_down_sync(0xffffffffu, nc[0].h, 1);
+            nb.u = __shfl_down_sync(0xffffffffu, nc[0].u, 1);
+            nb.v = __shfl_down_sync(0xffffffffu, nc[0].v, 1);
+            nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu, 1);
+            nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr, 1);
+            nb.fv = T(0);
+#pragma unroll
+            for (int i = 0; i < CPL - 1; ++i) nxr[i] = x_face<T, DM>(nc[i], nc[i + 1], c, ok);
+            nxr[CPL - 1] = x_face<T, DM>(nc[CPL - 1], nb, c, ok);
+            nxl.fh = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fh, 1);
+            nxl.fu = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fu, 1);
+            nxl.fv = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fv, 1);
+        }
+    }
+    template <int DM>
+    __device__ __forceinline__ void update(const Coef<T>& c, T (&oh)[CPL], T (&ou)[CPL], T (&ov)[CPL]) const {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i)
+            update_cell<T, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i], ydn[i], yup[i], c,
+                               oh[i], ou[i], ov[i]);
+    }
+    __device__ __forceinline__ void shift() {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) { pc[i] = nc[i]; ydn[i] = yup[i]; pxr[i] = nxr[i]; }
+        pxl = nxl;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// packed-pair arithmetic (fast mode: contraction into FFMA2 is intended)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 rcp2(float2 a) { return make_float2(rcp_approx(a.x), rcp_approx(a.y)); }
+
+struct CellQ2 {
+    float2 h, u, v, fu, fv, cr;
+    __device__ __forceinline__ CellQ<float> lo() const { return {h.x, u.x, v.x, fu.x, fv.x, cr.x}; }
+    __device__ __forceinline__ CellQ<float> hi() const { return {h.y, u.y, v.y, fu.y, fv.y, cr.y}; }
+};
+struct FaceF2 {
+    float2 fh, fu, fv;
+};
+struct Coef2 {
+    float2 half, cx2, cy2, cx, cy, g2;
+};
+
+// fxu(h,u) = u*u/h + g2*h*h, fxu(h,v), cross = u*v/h with one reciprocal
+__device__ __forceinline__ CellQ2 cell_q2(float2 h, float2 u, float2 v, const Coef2& c) {
+    CellQ2 q;
+    q.h = h; q.u = u; q.v = v;
+    const float2 r = rcp2(h);
+    const float2 uq = mul2(u, r), vq = mul2(v, r);
+    const float2 gh2 = mul2(mul2(c.g2, h), h);
+    q.fu = fma2(u, uq, gh2);
+    q.fv = fma2(v, vq, gh2);
+    q.cr = mul2(uq, v);
+    return q;
+}
+
+// y-faces between row cells D (below) and U (above), statements Hy, Uy, Vy
+__device__ __forceinline__ FaceF2 y_face2(const CellQ2& D, const CellQ2& U, const Coef2& c) {
+    const float2 Hy = fma2(c.cy2, sub2(D.v, U.v), mul2(c.half, add2(D.h, U.h)));
+    const float2 Uy = fma2(c.cy2, sub2(D.cr, U.cr), mul2(c.half, add2(D.u, U.u)));
+    const float2 Vy = fma2(c.cy2, sub2(D.fv, U.fv), mul2(c.half, add2(D.v, U.v)));
+    const float2 t = mul2(Vy, rcp2(Hy));
+    FaceF2 f;
+    f.fh = Vy;
+    f.fu = mul2(Uy, t);
+    f.fv = fma2(Vy, t, mul2(mul2(c.g2, Hy), Hy));
+    return f;
+}
+
+struct PairEngine {
+    static constexpr int CPL = 4;
+    CellQ2 pc[2];       // previous row: pairs (c0,c1), (c2,c3)
+    FaceF2 pdx[2];      // previous row: F_left - F_right of its x-faces, per cell
+    FaceF2 ydn[2];      // y-face below the previous row
+    CellQ2 nc[2];
+    FaceF2 ndx[2], yup[2];
+    Coef2 c2;
+
+    __device__ __forceinline__ void init(const Coef<float>& c) {
+        c2.half = bc2(c.half); c2.cx2 = bc2(c.cx2); c2.cy2 = bc2(c.cy2);
+        c2.cx = bc2(c.cx); c2.cy = bc2(c.cy); c2.g2 = bc2(c.g2);
+    }
+
+    template <int DM>
+    __device__ __forceinline__ void row(const VecF<float>& h, const VecF<float>& u, const VecF<float>& v,
+                                        bool have_prev, bool want_x, const Coef<float>& c, bool& ok) {
+        nc[0] = cell_q2(make_float2(h.v[0], h.v[1]), make_float2(u.v[0], u.v[1]), make_float2(v.v[0], v.v[1]), c2);
+        nc[1] = cell_q2(make_float2(h.v[2], h.v[3]), make_float2(u.v[2], u.v[3]), make_float2(v.v[2], v.v[3]), c2);
+        if (have_prev) {
+            yup[0] = y_face2(pc[0], nc[0], c2);
+            yup[1] = y_face2(pc[1], nc[1], c2);
+        }
+        if (want_x) {
+            CellQ<float> nb;  // first cell of lane+1
+            nb.h = __shfl_down_sync(0xffffffffu, nc[0].h.x, 1);
+            nb.u = __shfl_down_sync(0xffffffffu, nc[0].u.x, 1);
+            nb.v = __shfl_down_sync(0xffffffffu, nc[0].v.x, 1);
+            nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu.x, 1);
+            nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr.x, 1);
+            nb.fv = 0.f;
+            const FaceF<float> f01 = x_face<float, DIV_FAST>(nc[0].lo(), nc[0].hi(), c, ok);
+            const FaceF<float> f12 = x_face<float, DIV_FAST>(nc[0].hi(), nc[1].lo(), c, ok);
+            const FaceF<float> f23 = x_face<float, DIV_FAST>(nc[1].lo(), nc[1].hi(), c, ok);
+            const FaceF<float> f34 = x_face<float, DIV_FAST>(nc[1].hi(), nb, c, ok);
+            FaceF<float> fl;  // face left of c0 = lane-1's f34
+            fl.fh = __shfl_up_sync(0xffffffffu, f34.fh, 1);
+            fl.fu = __shfl_up_sync(0xffffffffu, f34.fu, 1);
+            fl.fv = __shfl_up_sync(0xffffffffu, f34.fv, 1);
+            ndx[0].fh = make_float2(fl.fh - f01.fh, f01.fh - f12.fh);
+            ndx[0].fu = make_float2(fl.fu - f01.fu, f01.fu - f12.fu);
+            ndx[0].fv = make_float2(fl.fv - f01.fv, f01.fv - f12.fv);
+            ndx[1].fh = make_float2(f12.fh - f23.fh, f23.fh - f34.fh);
+            ndx[1].fu = make_float2(f12.fu - f23.fu, f23.fu - f34.fu);
+            ndx[1].fv = make_float2(f12.fv - f23.fv, f23.fv - f34.fv);
+        }
+    }
+    // q' = (q + cx*(F_left - F_right)) + cy*(G_down - G_up)
+    template <int DM>
+    __device__ __forceinline__ void update(const Coef<float>&, float (&oh)[4], float (&ou)[4], float (&ov)[4]) const {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float2 h = fma2(c2.cy, sub2(ydn[j].fh, yup[j].fh), fma2(c2.cx, pdx[j].fh, pc[j].h));
+            const float2 u = fma2(c2.cy, sub2(ydn[j].fu, yup[j].fu), fma2(c2.cx, pdx[j].fu, pc[j].u));
+            const float2 v = fma2(c2.cy, sub2(ydn[j].fv, yup[j].fv), fma2(c2.cx, pdx[j].fv, pc[j].v));
+            oh[2 * j] = h.x; oh[2 * j + 1] = h.y;
+            ou[2 * j] = u.x; ou[2 * j + 1] = u.y;
+            ov[2 * j] = v.x; ov[2 * j + 1] = v.y;
+        }
+    }
+    __device__ __forceinline__ void shift() {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) { pc[j] = nc[j]; ydn[j] = yup[j]; pdx[j] = ndx[j]; }
+    }
+};
+
+}  // namespace fkc

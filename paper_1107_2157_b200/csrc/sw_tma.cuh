@@ -19,7 +19,7 @@
 // then updated and stored with vector stores; the output halo (boundary
 // conditions) and optional reductions are emitted in the same pass.
 #pragma once
-#include "sw_kernels.cuh"
+#include "sw_pair.cuh"
 
 namespace fkc {
 namespace tma {
@@ -56,6 +56,9 @@ template <class T> struct Geo {
 constexpr int THREADS = WARPS * 32;
 #ifndef FKC_EXACT_ALWAYS_FIXUP
 #define FKC_EXACT_ALWAYS_FIXUP 0
+#endif
+#ifndef FKC_TMA_PAIR
+#define FKC_TMA_PAIR 1        // f32 fast mode on the packed FP32 pipe (FFMA2 / FADD2 / FMUL2)
 #endif
 #ifndef FKC_EXACT_UNROLL
 #define FKC_EXACT_UNROLL 1
@@ -104,9 +107,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 
 // One lane's 16-byte vector of a row (4 floats or 2 doubles): shared-memory
 // load, global store.
-template <class T> struct VecF {
-    T v[16 / sizeof(T)];
-};
 template <class T>
 __device__ __forceinline__ VecF<T> lds_vec(uint32_t a) {
     VecF<T> r;
@@ -134,39 +134,6 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
     tma_load_2d(st, mH, tx, ty, bar);
     tma_load_2d(st + FB, mU, tx, ty, bar);
     tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
-}
-
-// Faces of one freshly loaded row: cell quantities nc, the y-faces between
-// the previous row pc and this row (if have_prev), and the x-faces of this
-// row (if want_x): nxr[i] = face between cell i and i+1 of the lane (cell
-// CPL comes from lane+1), nxl = face left of cell 0 (= nxr[CPL-1] of lane-1).
-template <class T, int DM, int CPL>
-__device__ __forceinline__ void row_faces(const VecF<T>& h, const VecF<T>& u, const VecF<T>& v,
-                                          const CellQ<T> (&pc)[CPL], bool have_prev, bool want_x,
-                                          const Coef<T>& c, CellQ<T> (&nc)[CPL],
-                                          FaceF<T> (&yup)[CPL], FaceF<T> (&nxr)[CPL],
-                                          FaceF<T>& nxl, bool& ok) {
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) nc[i] = cell_q<T, DM>(h.v[i], u.v[i], v.v[i], c, ok);
-    if (have_prev) {
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) yup[i] = y_face<T, DM>(pc[i], nc[i], c, ok);
-    }
-    if (want_x) {
-        CellQ<T> nb;  // first cell of lane+1
-        nb.h = __shfl_down_sync(0xffffffffu, nc[0].h, 1);
-        nb.u = __shfl_down_sync(0xffffffffu, nc[0].u, 1);
-        nb.v = __shfl_down_sync(0xffffffffu, nc[0].v, 1);
-        nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu, 1);
-        nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr, 1);
-        nb.fv = T(0);
-#pragma unroll
-        for (int i = 0; i < CPL - 1; ++i) nxr[i] = x_face<T, DM>(nc[i], nc[i + 1], c, ok);
-        nxr[CPL - 1] = x_face<T, DM>(nc[CPL - 1], nb, c, ok);
-        nxl.fh = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fh, 1);
-        nxl.fu = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fu, 1);
-        nxl.fv = __shfl_up_sync(0xffffffffu, nxr[CPL - 1].fv, 1);
-    }
 }
 
 // Tensor coordinates: the maps are encoded with base = &field(1 - CPL, 0)
@@ -251,9 +218,12 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const bool edge_cols = owner && ((X == 1) || (X + CPL - 1 == nx));
     const uint32_t lane_off = 16u * lane;
 
-    CellQ<T> pc[CPL];                  // previous row's cells
-    FaceF<T> pxl, pxr[CPL];            // previous row's x-face fluxes
-    FaceF<T> ydn[CPL];                 // y-face below the previous row
+    // the y-sweep's register window: packed-pair engine for f32 fast mode
+    // (sw_pair.cuh), scalar engine otherwise
+    constexpr bool PAIR = FAST && sizeof(T) == 4 && FKC_TMA_PAIR;
+    using Engine = typename std::conditional<PAIR, PairEngine, ScalarEngine<T, CPL>>::type;
+    Engine eng;
+    if constexpr (PAIR) eng.init(c);
     RedAcc<T> acc;
     acc.init();
     bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
@@ -290,11 +260,9 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             }
             const bool have_prev = n >= 1;
             const bool want_x = (n >= 1) && (n <= nrows);
-            CellQ<T> nc[CPL];
-            FaceF<T> yup[CPL], nxl, nxr[CPL];
             bool ok = true;
             if (FAST) {
-                row_faces<T, DIV_FAST, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                eng.template row<DIV_FAST>(hv, uv, vv, have_prev, want_x, c, ok);
             } else {
                 // exact mode, warp-uniform per row: lean guarded division;
                 // if any lane saw a non-benign operand, redo the row with the
@@ -304,14 +272,14 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 // fixup variant the next rows start with it and the lean
                 // variant is retried every 16 rows.
                 if (!fix_mode && !FKC_EXACT_ALWAYS_FIXUP) {
-                    row_faces<T, DIV_GUARD, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    eng.template row<DIV_GUARD>(hv, uv, vv, have_prev, want_x, c, ok);
                     if (__any_sync(0xffffffffu, !ok)) {
                         fix_mode = true;
                         fix_rows = 0;
-                        row_faces<T, DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                        eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
                     }
                 } else {
-                    row_faces<T, DIV_FIXUP, CPL>(hv, uv, vv, pc, have_prev, want_x, c, nc, yup, nxr, nxl, ok);
+                    eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
                     if (++fix_rows >= 16) fix_mode = false;
                 }
             }
@@ -319,10 +287,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             if (n >= 2 && n <= nrows + 1) {
                 const int y = down ? ytop - n + 1 : y0 + n - 2;
                 T oh[CPL], ou[CPL], ov[CPL];
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    update_cell<T, DM>(pc[i].h, pc[i].u, pc[i].v, i == 0 ? pxl : pxr[i - 1], pxr[i],
-                                           ydn[i], yup[i], c, oh[i], ou[i], ov[i]);
+                eng.template update<DM>(c, oh, ou, ov);
                 if (FAST) {
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) ov[i] *= vsign;   // back from the mirror image
@@ -386,9 +351,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 }
             }
             // shift the register window (renamed away by the unrolled loop)
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) { pc[i] = nc[i]; ydn[i] = yup[i]; pxr[i] = nxr[i]; }
-            pxl = nxl;
+            eng.shift();
         }
         __syncwarp();
     }
