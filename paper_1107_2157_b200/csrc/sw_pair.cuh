@@ -32,6 +32,17 @@ template <class T, int CPL> struct ScalarEngine {
     CellQ<T> nc[CPL];                  // new row
     FaceF<T> yup[CPL], nxl, nxr[CPL];
 
+    // benign window (a lake at rest) so a branch-free first row computes
+    // finite, discarded faces
+    __device__ __forceinline__ void init(const Coef<T>&) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            pc[i] = CellQ<T>{T(1), T(0), T(0), T(0), T(0), T(0)};
+            ydn[i] = pxr[i] = FaceF<T>{T(0), T(0), T(0)};
+        }
+        pxl = FaceF<T>{T(0), T(0), T(0)};
+    }
+
     template <int DM>
     __device__ __forceinline__ void row(const VecF<T>& h, const VecF<T>& u, const VecF<T>& v, bool have_prev,
                                         bool want_x, const Coef<T>& c, bool& ok) {
@@ -131,6 +142,14 @@ struct PairEngine {
     __device__ __forceinline__ void init(const Coef<float>& c) {
         c2.half = bc2(c.half); c2.cx2 = bc2(c.cx2); c2.cy2 = bc2(c.cy2);
         c2.cx = bc2(c.cx); c2.cy = bc2(c.cy); c2.g2 = bc2(c.g2);
+        // benign window (a lake at rest): a branch-free first row computes
+        // finite, discarded faces
+        const float2 one = bc2(1.f), zero = bc2(0.f);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            pc[j] = CellQ2{one, zero, zero, zero, zero, zero};
+            pdx[j] = ydn[j] = FaceF2{zero, zero, zero};
+        }
     }
 
     template <int DM>

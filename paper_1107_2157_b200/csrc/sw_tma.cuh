@@ -223,7 +223,11 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     constexpr bool PAIR = FAST && sizeof(T) == 4 && FKC_TMA_PAIR;
     using Engine = typename std::conditional<PAIR, PairEngine, ScalarEngine<T, CPL>>::type;
     Engine eng;
-    if constexpr (PAIR) eng.init(c);
+    eng.init(c);
+    // element offset of the row updated at loaded-row index n (lane's cell 0),
+    // advanced by one row per loaded row
+    const int64_t row_step = down ? -pitch : pitch;
+    int64_t row_off = (int64_t)(down ? ytop + 1 : y0 - 2) * pitch + X;
     RedAcc<T> acc;
     acc.init();
     bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
@@ -262,7 +266,9 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             const bool want_x = (n >= 1) && (n <= nrows);
             bool ok = true;
             if (FAST) {
-                eng.template row<DIV_FAST>(hv, uv, vv, have_prev, want_x, c, ok);
+                // branch-free: the faces of the first loaded row / of rows past the
+                // segment are computed on benign or discarded data, never stored
+                eng.template row<DIV_FAST>(hv, uv, vv, true, true, c, ok);
             } else {
                 // exact mode, warp-uniform per row: lean guarded division;
                 // if any lane saw a non-benign operand, redo the row with the
@@ -284,7 +290,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 }
             }
             // full-step update of the previous row (row y0 + n - 2; top-down: ytop - n + 1)
-            if (n >= 2 && n <= nrows + 1) {
+            const bool upd = (n >= 2) && (n <= nrows + 1);
+            if (FAST || upd) {
                 const int y = down ? ytop - n + 1 : y0 + n - 2;
                 T oh[CPL], ou[CPL], ov[CPL];
                 eng.template update<DM>(c, oh, ou, ov);
@@ -292,8 +299,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) ov[i] *= vsign;   // back from the mirror image
                 }
-                if (owner) {
-                    const int64_t off = (int64_t)y * pitch + X;
+                const int64_t off = row_off;
+                if (owner && upd) {
                     stg_vec<T, CPL>(oH + off, oh);
                     stg_vec<T, CPL>(oU + off, ou);
                     stg_vec<T, CPL>(oV + off, ov);
@@ -350,6 +357,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                     }
                 }
             }
+            row_off += row_step;
             // shift the register window (renamed away by the unrolled loop)
             eng.shift();
         }
