@@ -180,6 +180,10 @@ def main():
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1 halo exchange: peer = fused into the step kernel over NVLink peer memory "
                          "(CUDA IPC + mailbox flags); nccl = pack + NCCL send/recv + unpack (baseline)")
+    ap.add_argument("--diag", default="none", choices=["none", "diag", "cfl"],
+                    help="fused reductions in the timed steps: none; diag = mass, max|hu|, max|hv|, error word "
+                         "(run()'s per-step diagnostics); cfl = diag + the CFL bound, dt recomputed on device "
+                         "every step (SPEC.md:529-537 run)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the other-mode timing (profiling runs)")
@@ -228,7 +232,7 @@ def main():
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0
     r = time_steps(st, n, dt, args.mode, args.variant, args.steps, args.warmup, sample_clocks=True,
-                   precision=args.precision)
+                   precision=args.precision, diag=args.diag)
     total_ms, per_launch, clocks = r["total_ms"], r["per_launch"], r["clocks"]
     ms_step = total_ms / args.steps
     cells = n * n
@@ -264,7 +268,7 @@ def main():
         "data": "synthetic (Gaussian hump h=1+0.4exp(-r^2/(n/8)^2), hu=hv=0)",
         "config": {"workload": f"shallow-water {n}x{n} {'fp32' if args.precision == 'f32' else 'fp64'}, reflective, "
                                f"fixed dt=0.3*stable_dt (BASELINE config 3)",
-                   "precision": args.precision,
+                   "precision": args.precision, "diagnostics": args.diag,
                    "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else
                    f"rtol {FAST_RTOL} vs oracle (tests/test_gpu_parity.py)",
                    "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",
@@ -293,16 +297,16 @@ def main():
     return 0
 
 
-def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32"):
+def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32", diag="none"):
     """K steps of the fused step kernel, CUDA events on the launching stream
     (one event pair per launch: the step kernel is the only launch)."""
     import torch
     from paper_1107_2157_b200 import swdemo
-    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps + warmup, dt=dt, mode=mode, variant=variant,
-                          precision=precision)
+    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps + warmup, dt=None if diag == "cfl" else dt, mode=mode,
+                          variant=variant, precision=precision, cfl_factor=0.3)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+        sim = swdemo.Simulation(cfg, state=st, diagnostics=diag != "none", stream=stream)
         sim.advance(warmup)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
@@ -320,6 +324,8 @@ def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, pre
         torch.cuda.synchronize()
         if clocks:
             clocks.__exit__(None, None, None)
+    if diag != "none":
+        sim.rows()                      # raises NonfiniteValue / NonPositiveDepth from the error words
     fin = sim.state()
     assert bool(torch.isfinite(fin.H.data).all().item()), "non-finite state after the timed run"
     return {"total_ms": t_start.elapsed_time(t_end), "steps": steps,

@@ -230,7 +230,7 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     return seg;
 }
 
-template <class T, bool FAST, bool RED>
+template <class T, bool FAST, int RED>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
     using G = tma::Geo<T>;
     static bool attr_set = false;
@@ -260,9 +260,15 @@ int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
     for (int f = 0; f < 3; ++f)
         if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<T>::LOAD, (int)sizeof(T), &m[f]))) return rc;
     const bool fast = a->mode == FKC_MODE_FAST;
-    const bool r = any_red(to_red(a->red));
-    if (fast) return r ? launch_tma_t<T, true, true>(a, st, m) : launch_tma_t<T, true, false>(a, st, m);
-    return r ? launch_tma_t<T, false, true>(a, st, m) : launch_tma_t<T, false, false>(a, st, m);
+    // reduction level: 0 none, 1 mass / maxima / error word, 2 + CFL bound
+    const RedPtrs rp = to_red(a->red);
+    const int lvl = rp.cfl_min ? 2 : (any_red(rp) ? 1 : 0);
+    if (fast) {
+        if (lvl == 2) return launch_tma_t<T, true, 2>(a, st, m);
+        return lvl ? launch_tma_t<T, true, 1>(a, st, m) : launch_tma_t<T, true, 0>(a, st, m);
+    }
+    if (lvl == 2) return launch_tma_t<T, false, 2>(a, st, m);
+    return lvl ? launch_tma_t<T, false, 1>(a, st, m) : launch_tma_t<T, false, 0>(a, st, m);
 }
 
 int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {

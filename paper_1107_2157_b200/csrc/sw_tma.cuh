@@ -60,6 +60,9 @@ constexpr int THREADS = WARPS * 32;
 #ifndef FKC_TMA_PAIR
 #define FKC_TMA_PAIR 1        // f32 fast mode on the packed FP32 pipe (FFMA2 / FADD2 / FMUL2)
 #endif
+#ifndef FKC_FAST_UNROLL
+#define FKC_FAST_UNROLL 2     // rows of a stage unrolled in fast mode (even: the register window renames)
+#endif
 #ifndef FKC_EXACT_UNROLL
 #define FKC_EXACT_UNROLL 1
 #endif
@@ -136,17 +139,66 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
     tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
 }
 
+template <class T, int CPL> struct Row3 {
+    T h[CPL], u[CPL], v[CPL];
+};
+
+// Output halo of one new row segment of CPL cells (x = X .. X+CPL-1, row y)
+// on the tile edge: reflective / periodic images (apply_boundary of the new
+// state, corners included) and the neighbour tiles' halo lines (fused
+// exchange).  Rare (edge lanes only), so it lives out of the sweep loop.
+template <class T, int CPL>
+__device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int nx, int ny, int X, int y,
+                                         const BCs& bc, const Peers& P, Row3<T, CPL> o) {
+    if (y == 1 || y == ny) {
+        const bool refl = (y == 1 && bc.s[SIDE_D] == BC_REFL) || (y == ny && bc.s[SIDE_U] == BC_REFL);
+        const bool per = (y == 1 && bc.s[SIDE_U] == BC_PER) || (y == ny && bc.s[SIDE_D] == BC_PER);
+        if (refl) {
+            const int64_t o2 = (int64_t)(y == 1 ? 0 : ny + 1) * pitch + X;
+            stg_vec<T, CPL>(oH + o2, o.h);
+            stg_vec<T, CPL>(oU + o2, o.u);
+            stg_vec<T, CPL>(oV + o2, o.v, T(-1));
+        }
+        if (per) {
+            const int64_t o2 = (int64_t)(y == 1 ? ny + 1 : 0) * pitch + X;
+            stg_vec<T, CPL>(oH + o2, o.h);
+            stg_vec<T, CPL>(oU + o2, o.u);
+            stg_vec<T, CPL>(oV + o2, o.v);
+        }
+        // fused halo exchange: the new row goes straight into the neighbour
+        // tile's halo row (row lines: stride 1)
+#pragma unroll
+        for (int side = SIDE_D; side <= SIDE_U; ++side) {
+            const PeerLine& pl = P.s[side];
+            if (pl.p[0] && (side == SIDE_D ? y == 1 : y == ny)) {
+                stg_vec<T, CPL>((T*)pl.p[0] + X, o.h);
+                stg_vec<T, CPL>((T*)pl.p[1] + X, o.u);
+                stg_vec<T, CPL>((T*)pl.p[2] + X, o.v);
+            }
+        }
+    }
+    if (X == 1) {
+        emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, 1, y, o.h[0], o.u[0], o.v[0], false);
+        if (P.s[SIDE_L].p[0]) peer_store<T>(P.s[SIDE_L], y, o.h[0], o.u[0], o.v[0]);
+    }
+    if (X + CPL - 1 == nx) {
+        emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, nx, y, o.h[CPL - 1], o.u[CPL - 1], o.v[CPL - 1], false);
+        if (P.s[SIDE_R].p[0]) peer_store<T>(P.s[SIDE_R], y, o.h[CPL - 1], o.u[CPL - 1], o.v[CPL - 1]);
+    }
+}
+
 // Tensor coordinates: the maps are encoded with base = &field(1 - CPL, 0)
 // so that full-array column x is tensor column x + CPL - 1 (16-B aligned
 // boxes: cell 1 is 128-B aligned).  Strip j owns columns
 // [1 + OWN j, OWN (j+1)] and loads full columns [1 + OWN j - CPL,
 // OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
-template <class T, bool FAST, bool RED>
+template <class T, bool FAST, int RED>
 __global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg, int alt,
             T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
-            T dx, T dy, DtSrc dts, T g, BCs bc, RedPtrs red, Peers P, SyncArgs sy) {
+            T dx, T dy, DtSrc dts, T g, const __grid_constant__ BCs bc, RedPtrs red,
+            const __grid_constant__ Peers P, SyncArgs sy) {
     using namespace tma;
     using G = Geo<T>;
     constexpr int CPL = G::CPL;
@@ -228,11 +280,11 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     // advanced by one row per loaded row
     const int64_t row_step = down ? -pitch : pitch;
     int64_t row_off = (int64_t)(down ? ytop + 1 : y0 - 2) * pitch + X;
-    RedAcc<T> acc;
-    acc.init();
+    RowRed<T, FAST, RED> rr;
+    rr.init();
     bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
     int fix_rows = 0;
-    constexpr int UNR = FAST ? R : FKC_EXACT_UNROLL;  // exact: keep the loop body inside the I-cache
+    constexpr int UNR = FAST ? FKC_FAST_UNROLL : FKC_EXACT_UNROLL;  // keep the loop body inside the I-cache
 
     for (int k = 0; k < nstages; ++k) {
         const int s = k % tma::S;
@@ -304,57 +356,15 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                     stg_vec<T, CPL>(oH + off, oh);
                     stg_vec<T, CPL>(oU + off, ou);
                     stg_vec<T, CPL>(oV + off, ov);
-                    // fused boundary fill of the output halo
-                    if (edge_rows && (y == 1 || y == ny)) {
-                        const bool refl = (y == 1 && bc.s[SIDE_D] == BC_REFL) || (y == ny && bc.s[SIDE_U] == BC_REFL);
-                        const bool per = (y == 1 && bc.s[SIDE_U] == BC_PER) || (y == ny && bc.s[SIDE_D] == BC_PER);
-                        if (refl) {
-                            const int64_t o2 = (int64_t)(y == 1 ? 0 : ny + 1) * pitch + X;
-                            stg_vec<T, CPL>(oH + o2, oh);
-                            stg_vec<T, CPL>(oU + o2, ou);
-                            stg_vec<T, CPL>(oV + o2, ov, T(-1));
-                        }
-                        if (per) {
-                            const int64_t o2 = (int64_t)(y == 1 ? ny + 1 : 0) * pitch + X;
-                            stg_vec<T, CPL>(oH + o2, oh);
-                            stg_vec<T, CPL>(oU + o2, ou);
-                            stg_vec<T, CPL>(oV + o2, ov);
-                        }
-                        // fused halo exchange: the new row goes straight into
-                        // the neighbour tile's halo row (rows: stride 1)
-                        const PeerLine& pl = P.s[y == 1 ? SIDE_D : SIDE_U];
-                        if (pl.p[0]) {
-                            stg_vec<T, CPL>((T*)pl.p[0] + X, oh);
-                            stg_vec<T, CPL>((T*)pl.p[1] + X, ou);
-                            stg_vec<T, CPL>((T*)pl.p[2] + X, ov);
-                        }
-                        if (y == 1 && y == ny && P.s[SIDE_U].p[0]) {   // single-row tile
-                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[0] + X, oh);
-                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[1] + X, ou);
-                            stg_vec<T, CPL>((T*)P.s[SIDE_U].p[2] + X, ov);
-                        }
-                    }
-                    if (edge_cols) {
-                        if (X == 1) {
-                            emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, 1, y, oh[0], ou[0], ov[0], false);
-                            if (P.s[SIDE_L].p[0]) peer_store<T>(P.s[SIDE_L], y, oh[0], ou[0], ov[0]);
-                        }
-                        if (X + CPL - 1 == nx) {
-                            emit_halos<T>(oH, oU, oV, pitch, nx, ny, bc, nx, y, oh[CPL - 1], ou[CPL - 1],
-                                          ov[CPL - 1], false);
-                            if (P.s[SIDE_R].p[0])
-                                peer_store<T>(P.s[SIDE_R], y, oh[CPL - 1], ou[CPL - 1], ov[CPL - 1]);
-                        }
-                    }
-                    if (RED) {
-                        double m = 0.0;
+                    // output halo (boundary conditions) and fused halo exchange:
+                    // tile-edge lanes only, out of line to keep the sweep loop small
+                    if ((edge_rows && (y == 1 || y == ny)) || edge_cols) {
+                        Row3<T, CPL> o;
 #pragma unroll
-                        for (int i = 0; i < CPL; ++i) m += (double)oh[i];
-                        acc.mass += m;
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i)
-                            acc.add_cell(oh[i], ou[i], ov[i], g, dmin, red.cfl_min != nullptr, red.err != nullptr);
+                        for (int i = 0; i < CPL; ++i) { o.h[i] = oh[i]; o.u[i] = ou[i]; o.v[i] = ov[i]; }
+                        edge_stores<T, CPL>(oH, oU, oV, pitch, nx, ny, X, y, bc, P, o);
                     }
+                    if constexpr (RED > 0) rr.template add_row<CPL>(oh, ou, ov, g);
                 }
             }
             row_off += row_step;
@@ -370,7 +380,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         const int expected[4] = {(int)gridDim.y, (int)gridDim.y, nstrips, nstrips};
         if (lane == 0) peer_signal(sy, sides, expected);
     }
-    if (RED) warp_reduce_commit<T>(acc, red, lane);
+    if constexpr (RED > 0) rr.commit(red, lane, dmin);
 }
 
 }  // namespace fkc
