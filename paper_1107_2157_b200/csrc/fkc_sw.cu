@@ -372,8 +372,8 @@ int fkc_sw_reduce_state(const fkc_grid* g, const void* H, const void* U, const v
     if (!H || !U || !V || !red) return fail(FKC_EUSAGE, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     const double dmin = dx < dy ? dx : dy;
-    int blocks = (int)(((int64_t)g->nx * g->ny + 255) / 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    int blocks = (g->ny + 7) / 8;                 // 8 warps (rows in flight) per block
+    if (blocks > 148 * 8) blocks = 148 * 8;
     if (g->dtype == FKC_F32)
         sw_reduce_kernel<float><<<blocks, 256, 0, st>>>(g->nx, g->ny, g->pitch, (const float*)H, (const float*)U,
                                                         (const float*)V, (float)gravity, (float)dmin, to_red(*red));
