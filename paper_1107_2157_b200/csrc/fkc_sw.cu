@@ -319,7 +319,12 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (int rc = valid_peers(a)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     int variant = a->variant;
-    if (variant == FKC_VARIANT_AUTO) variant = tma_eligible(a) ? FKC_VARIANT_TMA : FKC_VARIANT_GENERIC;
+    // AUTO: the TMA sweep for grids of >= 2^21 cells (HBM regime); below that
+    // (L2-resident / launch-bound) the generic kernel's one-thread-per-cell
+    // parallelism wins -- B200 grid sweep, profiles/r01/grid_sweep.json
+    if (variant == FKC_VARIANT_AUTO)
+        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(1) << 21) ? FKC_VARIANT_TMA
+                                                                                              : FKC_VARIANT_GENERIC;
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
             return fail(FKC_EUSAGE, "TMA variant needs nx and pitch multiples of 16/elem_size and (ptr+1 elem) "

@@ -152,7 +152,7 @@ def test_local_decomposed_gpu_bit_identical(px, py, bc, mode, exchange):
     from paper_1107_2157_b200 import swdemo
     from paper_1107_2157_b200.decomp import run_local_decomposed
     nx, ny, steps = 960, 512, 8
-    cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode)
+    cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode, variant="tma")
     grid, states = run_local_decomposed(cfg, px, py, steps, exchange=exchange.split("-")[0],
                                         concurrent=exchange.endswith("concurrent"))
     sim = swdemo.Simulation(cfg, diagnostics=False)
@@ -232,7 +232,7 @@ def _peer_worker(rank, world, port, px, py, nx, ny, steps, bc, mode, q):
     try:
         torch.cuda.set_device(0)
         grid = CartGrid(px, py, nx, ny, bc)
-        cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode)
+        cfg = swdemo.SWConfig(nx=nx, ny=ny, dt=0.05, boundary=bc, mode=mode, variant="tma")
         sim = DistributedSimulation(cfg, grid, rank, torch.device("cuda", 0), transport="peer")
         sim.advance(steps)
         torch.cuda.synchronize()
