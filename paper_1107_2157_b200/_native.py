@@ -24,7 +24,7 @@ VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA = 0, 1, 2
 ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
 
 EXPORTS = (
-    "fkc_sw_step", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
+    "fkc_sw_step", "fkc_sw_advance_n", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
     "fkc_ipc_export", "fkc_ipc_open", "fkc_ipc_close",
     "fkc_set_tma_segment", "fkc_set_tma_alternate", "fkc_test_div_f32", "fkc_last_error", "fkc_abi_version",
@@ -75,6 +75,13 @@ class StepArgs(ctypes.Structure):
                 ("red", Reduce), ("peer", PeerLine * 4), ("sync", Sync)]
 
 
+class LoopArgs(ctypes.Structure):
+    """fkc_sw_loop_args: the native time loop (fkc_sw_advance_n)."""
+    _fields_ = [("step", StepArgs), ("first_step", ctypes.c_int64), ("steps", ctypes.c_int64),
+                ("slots", ctypes.c_void_p), ("dt_from_slots", ctypes.c_int32), ("want_cfl", ctypes.c_int32),
+                ("use_graph", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
 _lib = None
 
 
@@ -100,6 +107,7 @@ def lib():
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     sig = {
         "fkc_sw_step": [ctypes.POINTER(StepArgs), vp],
+        "fkc_sw_advance_n": [ctypes.POINTER(LoopArgs), vp],
         "fkc_sw_apply_boundary": [ctypes.POINTER(Grid), vp, vp, vp, ctypes.POINTER(i32), vp],
         "fkc_sw_reduce_state": [ctypes.POINTER(Grid), vp, vp, vp, dbl, dbl, dbl,
                                 ctypes.POINTER(Reduce), vp],

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/fkc_sw.h"
@@ -333,6 +334,83 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     }
     if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");
     return a->grid.dtype == FKC_F32 ? launch_generic<float>(a, st) : launch_generic<double>(a, st);
+}
+
+// ---------------------------------------------------------------------------
+// native time loop (+ cached CUDA graphs)
+// ---------------------------------------------------------------------------
+static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
+    fkc_sw_step_args a = L->step;
+    const void* A[3] = {L->step.H, L->step.U, L->step.V};
+    void* B[3] = {L->step.oH, L->step.oU, L->step.oV};
+    for (int64_t k = 0; k < L->steps; ++k) {
+        const int64_t i = L->first_step + k;
+        const bool even = (i & 1) == 0;
+        a.H = even ? A[0] : B[0]; a.U = even ? A[1] : B[1]; a.V = even ? A[2] : B[2];
+        a.oH = even ? B[0] : (void*)A[0]; a.oU = even ? B[1] : (void*)A[1]; a.oV = even ? B[2] : (void*)A[2];
+        if (L->slots) {
+            uint64_t* in = L->slots + 5 * i;
+            uint64_t* out = L->slots + 5 * (i + 1);
+            a.red.mass = (double*)out;
+            a.red.max_abs_u = out + 1;
+            a.red.max_abs_v = out + 2;
+            a.red.cfl_min = L->want_cfl ? out + 3 : nullptr;
+            a.red.err = (uint32_t*)(out + 4);
+            a.dt_bound = L->dt_from_slots ? in + 3 : nullptr;
+        }
+        if (int rc = fkc_sw_step(&a, st)) return rc;
+    }
+    return FKC_OK;
+}
+
+struct GraphEntry {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec;
+};
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;
+
+int fkc_sw_advance_n(const fkc_sw_loop_args* L, void* stream) {
+    if (!L) return fail(FKC_EUSAGE, "null args");
+    if (L->steps < 0 || L->first_step < 0) return fail(FKC_EUSAGE, "steps and first_step must be >= 0");
+    if (L->step.sync.counter || L->step.peer[0].p[0] || L->step.peer[1].p[0] || L->step.peer[2].p[0] ||
+        L->step.peer[3].p[0])
+        return fail(FKC_EUSAGE, "fkc_sw_advance_n: peer lines / sync are per-step (use fkc_sw_step)");
+    if (L->dt_from_slots && !L->slots) return fail(FKC_EUSAGE, "dt_from_slots needs slots");
+    if (L->steps == 0) return FKC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!L->use_graph) return enqueue_loop(L, st);
+    // graph path: key = the whole argument block (pointers, dt, steps, parity...)
+    std::vector<unsigned char> key((const unsigned char*)L, (const unsigned char*)L + sizeof(*L));
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto& e : g_graphs)
+        if (e.key == key) {
+            cudaError_t err = cudaGraphLaunch(e.exec, st);
+            if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(err));
+            return FKC_OK;
+        }
+    cudaError_t err = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(err));
+    const int rc = enqueue_loop(L, st);
+    cudaGraph_t graph = nullptr;
+    err = cudaStreamEndCapture(st, &graph);
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(err));
+    cudaGraphExec_t exec = nullptr;
+    err = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(err));
+    if (g_graphs.size() >= 16) {
+        cudaGraphExecDestroy(g_graphs.front().exec);
+        g_graphs.erase(g_graphs.begin());
+    }
+    g_graphs.push_back({key, exec});
+    err = cudaGraphLaunch(exec, st);
+    if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(err));
+    return FKC_OK;
 }
 
 int fkc_sw_apply_boundary(const fkc_grid* g, void* H, void* U, void* V, const int32_t bc[4], void* stream) {

@@ -361,49 +361,57 @@ class Simulation:
         self._args = [None, None]
         self.torch = torch
 
-    def _args_for(self, i: int) -> N.StepArgs:
-        src, dst = (self.a, self.b) if i % 2 == 0 else (self.b, self.a)
+    def _loop_args(self, first: int, steps: int, use_graph: bool = False) -> N.LoopArgs:
+        """Argument block of the native time loop (fkc_sw_advance_n): buffer
+        A = self.a, B = self.b, global step index `first`, per-step
+        reduction rows in self.slots (row i+1 = state after step i)."""
         cfg = self.cfg
-        red = self.slots.reduce_struct(i + 1, cfl=cfg.dt is None) if self.diag else None
-        bound = self.slots.addr(i, 3) if cfg.dt is None else None
-        return _step_args(src, dst, cfg.dt if cfg.dt is not None else 0.0, self.boundary, cfg.mode,
-                          cfg.variant, red, bound, cfg.cfl_factor)
+        L = N.LoopArgs()
+        L.step = _step_args(self.a, self.b, cfg.dt if cfg.dt is not None else 0.0, self.boundary, cfg.mode,
+                            cfg.variant, None, None, cfg.cfl_factor)
+        L.first_step = first
+        L.steps = steps
+        if self.diag:
+            L.slots = self.slots.buf.data_ptr()
+            L.dt_from_slots = int(cfg.dt is None)
+            L.want_cfl = int(cfg.dt is None)
+        L.use_graph = int(use_graph)
+        return L
 
     def advance(self, steps: int):
+        """Enqueue `steps` steps with ONE native call (the loop runs in C,
+        fkc_sw_advance_n); no host synchronisation."""
         if self.diag and self.n + steps >= self.slots.n:
             raise ValueError("reduction slot capacity exceeded")
-        L = N.lib()
-        sp = _stream_ptr(self.stream)
-        for _ in range(steps):
-            a = self._args_for(self.n)
-            N.check(L.fkc_sw_step(ctypes.byref(a), sp))
-            self.n += 1
+        if steps <= 0:
+            return self
+        L = self._loop_args(self.n, steps)
+        N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), _stream_ptr(self.stream)))
+        self.n += steps
         return self
 
     def capture(self, steps: int):
         """CUDA-graph the next `steps` steps (fixed dt, no diagnostics) for
         launch-bound small grids: returns a callable that replays them.
         `steps` must be even so the double buffers end where they started;
-        each replay advances the state by `steps` steps."""
+        each replay advances the state by `steps` steps.  The graph is built
+        and cached natively (fkc_sw_advance_n with use_graph)."""
         torch = self.torch
         if steps % 2 or self.diag:
             raise ValueError("capture needs an even step count and diagnostics off")
         stream = self.stream if self.stream is not None else torch.cuda.Stream()
         self.advance(2)                      # warm-up outside capture (tensor maps, attributes)
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        n0 = self.n
-        with torch.cuda.graph(graph, stream=stream):
-            L = N.lib()
-            sp = stream.cuda_stream
-            for k in range(steps):
-                a = self._args_for(n0 + k)
-                N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+        parity = self.n % 2
+        L = self._loop_args(parity, steps, use_graph=True)
+        sp = stream.cuda_stream
+        N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), sp))     # capture + first launch
+        self.n += steps
 
         def replay():
-            graph.replay()
+            N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), sp))
             self.n += steps
-        replay.graph = graph
+        replay.args = L
         return replay
 
     def state(self) -> SWState:

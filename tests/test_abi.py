@@ -61,6 +61,21 @@ def test_usage_errors_without_gpu():
     a.sync.wait[0] = 1 << 21
     assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
     assert b"together" in L.fkc_last_error()
+    # native time loop: argument checks before any device work
+    assert L.fkc_sw_advance_n(None, None) == N.FKC_EUSAGE
+    la = N.LoopArgs()
+    la.steps = -1
+    assert L.fkc_sw_advance_n(ctypes.byref(la), None) == N.FKC_EUSAGE
+    la.steps = 3
+    la.step.sync.counter = 1 << 20
+    assert L.fkc_sw_advance_n(ctypes.byref(la), None) == N.FKC_EUSAGE
+    assert b"per-step" in L.fkc_last_error()
+    la.step.sync.counter = None
+    la.dt_from_slots = 1
+    assert L.fkc_sw_advance_n(ctypes.byref(la), None) == N.FKC_EUSAGE
+    la.dt_from_slots = 0
+    la.steps = 0
+    assert L.fkc_sw_advance_n(ctypes.byref(la), None) == N.FKC_OK       # nothing to do
 
 
 def test_struct_layout_matches_header():
@@ -76,6 +91,9 @@ def test_struct_layout_matches_header():
       printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_peer_line), sizeof(fkc_sync),
              offsetof(fkc_sw_step_args, peer), offsetof(fkc_sw_step_args, sync),
              offsetof(fkc_sync, counter), offsetof(fkc_sync, epoch));
+      printf("%zu %zu %zu %zu %zu\n", sizeof(fkc_sw_loop_args), offsetof(fkc_sw_loop_args, first_step),
+             offsetof(fkc_sw_loop_args, slots), offsetof(fkc_sw_loop_args, want_cfl),
+             offsetof(fkc_sw_loop_args, use_graph));
       return 0;
     }
     """
@@ -90,7 +108,9 @@ def test_struct_layout_matches_header():
     want = [ctypes.sizeof(N.Grid), ctypes.sizeof(N.Reduce), ctypes.sizeof(S),
             S.H.offset, S.dx.offset, S.dt_bound.offset, S.bc.offset, S.variant.offset, S.red.offset,
             ctypes.sizeof(N.PeerLine), ctypes.sizeof(N.Sync), S.peer.offset, S.sync.offset,
-            N.Sync.counter.offset, N.Sync.epoch.offset]
+            N.Sync.counter.offset, N.Sync.epoch.offset,
+            ctypes.sizeof(N.LoopArgs), N.LoopArgs.first_step.offset, N.LoopArgs.slots.offset,
+            N.LoopArgs.want_cfl.offset, N.LoopArgs.use_graph.offset]
     assert got == want
 
 
