@@ -30,7 +30,10 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_CELL = {"f32": 24, "f64": 48}      # read H,U,V + write oH,oU,oV
 FALLBACK_HBM_GBS = 6650.0
-FAST_RTOL = 2e-5          # fast-mode tolerance vs the oracle (tests/test_gpu_parity.py)
+FAST_RTOL = 2e-5          # fast-mode tolerance vs the oracle, 256^2 / 1024^2 (tests/test_gpu_parity.py)
+FAST_PARITY = ("fast: error vs the f64 solution within 1.1x that of the bit-exact f32 oracle, per field "
+               "(16384^2, 20 steps: both ~6e-4 normwise on hu, hv); rtol 2e-5 vs the f32 oracle at 256^2 "
+               "(tests/test_gpu_parity.py)")
 
 
 def peaks():
@@ -169,7 +172,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", "--grid-n", dest="n", type=int, default=16384, help="cells per side (per GPU)")
     ap.add_argument("--mode", default="fast", choices=["exact", "fast"],
-                    help="fast: FMA + approximate reciprocals, rtol 2e-5 vs the oracle (headline); "
+                    help="fast: FMA + approximate reciprocals, as accurate as the f32 oracle (headline); "
                          "exact: bit-identical to the oracle")
     ap.add_argument("--variant", default="auto", choices=["auto", "tma", "generic"])
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
@@ -249,7 +252,7 @@ def main():
         del st2
         other_line = {"mode": other, "value": round(cells * r2["steps"] / (r2["total_ms"] / 1e3) / 1e9, 3),
                       "ms_per_step": round(r2["total_ms"] / r2["steps"], 5), "steps": r2["steps"],
-                      "parity": "bit-exact vs oracle" if other == "exact" else f"rtol {FAST_RTOL} vs oracle"}
+                      "parity": "bit-exact vs oracle" if other == "exact" else FAST_PARITY}
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -269,8 +272,7 @@ def main():
         "config": {"workload": f"shallow-water {n}x{n} {'fp32' if args.precision == 'f32' else 'fp64'}, reflective, "
                                f"fixed dt=0.3*stable_dt (BASELINE config 3)",
                    "precision": args.precision, "diagnostics": args.diag,
-                   "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else
-                   f"rtol {FAST_RTOL} vs oracle (tests/test_gpu_parity.py)",
+                   "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else FAST_PARITY,
                    "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",
                    "l2": f"working set {BYTES_PER_CELL[args.precision] * (n + 2) * (n + 2) / 1e9:.1f} GB >> "
                          "126 MB L2 (no flush needed)"},
