@@ -317,7 +317,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             const bool have_prev = n >= 1;
             const bool want_x = (n >= 1) && (n <= nrows);
             bool ok = true;
-            if (FAST) {
+            if constexpr (FAST) {
                 // branch-free: the faces of the first loaded row / of rows past the
                 // segment are computed on benign or discarded data, never stored
                 eng.template row<DIV_FAST>(hv, uv, vv, true, true, c, ok);
