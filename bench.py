@@ -103,9 +103,10 @@ class ClockSampler:
 # CPU reference (oracle port) -- only used for the cpu_baseline / --impl reference legs
 # ---------------------------------------------------------------------------
 
-def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads=None):
+def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads=None, warmup=2):
     """Time the C restatement of the reference CPU path (all host threads)
-    on a bounded slab n x rows of the same workload."""
+    on a bounded slab n x rows of the same workload; `warmup` untimed steps
+    first (page faults of fresh buffers, thread start-up)."""
     from oracle import c_oracle
     from oracle import sw_oracle as so
     threads = threads or len(os.sched_getaffinity(0))
@@ -113,6 +114,9 @@ def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads
     dt = 0.3 * so.stable_dt(H, U, V, 1.0, 1.0)
     a = (H, U, V)
     b = tuple(np.empty_like(x) for x in a)
+    for _ in range(warmup):
+        c_oracle.step(*a, 1.0, 1.0, dt, out=b, threads=threads)
+        a, b = b, a
     times = []
     t_start = time.perf_counter()
     while len(times) < max_steps and (len(times) < min_steps or time.perf_counter() - t_start < budget_s):
@@ -202,8 +206,8 @@ def main():
             return 0
         rows = 1024
         cores = len(os.sched_getaffinity(0))
-        r = cpu_port_sample(n, rows, budget_s=1e9, min_steps=args.warmup + args.steps,
-                            max_steps=args.warmup + args.steps, threads=cores)
+        r = cpu_port_sample(n, rows, budget_s=1e9, min_steps=args.steps, max_steps=args.steps, threads=cores,
+                            warmup=args.warmup)
         line = {"metric": "Gcell-updates/s", "value": r["value"], "unit": "Gcell-updates/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",

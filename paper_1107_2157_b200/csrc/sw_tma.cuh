@@ -33,6 +33,9 @@ constexpr int WARPS = 4;                 // warps (strips) per CTA
 #ifndef FKC_TMA_CTAS_FAST
 #define FKC_TMA_CTAS_FAST 3   // fast kernel: <= 168 registers -> 12 warps per SM
 #endif
+#ifndef FKC_TMA_CTAS_FAST_RED
+#define FKC_TMA_CTAS_FAST_RED 3  // fast kernel with fused reductions
+#endif
 #ifndef FKC_TMA_CTAS_EXACT
 #define FKC_TMA_CTAS_EXACT 2  // exact kernel: ~190 registers -> 8 warps per SM
 #endif
@@ -48,8 +51,8 @@ template <class T> struct Geo {
     static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
     static constexpr int WARP_RING = S * STAGE_BYTES;
     static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
-    template <bool FAST> static constexpr int ctas_per_sm() {
-        return sizeof(T) == 8 ? 2 : (FAST ? FKC_TMA_CTAS_FAST : FKC_TMA_CTAS_EXACT);
+    template <bool FAST, int RED = 0> static constexpr int ctas_per_sm() {
+        return sizeof(T) == 8 ? 2 : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT);
     }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
@@ -193,7 +196,7 @@ __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int
 // [1 + OWN j, OWN (j+1)] and loads full columns [1 + OWN j - CPL,
 // OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
 template <class T, bool FAST, int RED>
-__global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST>())
+__global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST, RED>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg, int alt,
             T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
