@@ -36,6 +36,20 @@ FAST_PARITY = ("fast: error vs the f64 solution within 1.1x that of the bit-exac
                "(tests/test_gpu_parity.py)")
 
 
+METRIC = "Gcell-updates/s (shallow-water step)"
+
+
+def workload(n, world=1, precision="f32"):
+    """The workload string both arms report (BASELINE configs 3 / 5)."""
+    fp = "fp32" if precision == "f32" else "fp64"
+    if world == 1:
+        return f"shallow-water {n}x{n} {fp}, reflective, fixed dt=0.3*stable_dt (BASELINE config 3)"
+    from paper_1107_2157_b200.decomp import choose_grid
+    px, py = choose_grid(world)
+    return (f"shallow-water {n}x{n} {fp} per GPU ({px * n}x{py * n} global, 2-D decomposed {px}x{py}), "
+            f"reflective, fixed dt=0.3*stable_dt (BASELINE config 5, weak scaling)")
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -208,12 +222,12 @@ def main():
         cores = len(os.sched_getaffinity(0))
         r = cpu_port_sample(n, rows, budget_s=1e9, min_steps=args.steps, max_steps=args.steps, threads=cores,
                             warmup=args.warmup)
-        line = {"metric": "Gcell-updates/s", "value": r["value"], "unit": "Gcell-updates/s",
+        line = {"metric": METRIC, "value": r["value"], "unit": "Gcell-updates/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
-                "config": {"workload": f"shallow-water {n}x{n} fp32 reflective, fixed dt (sampled {n}x{rows} slab)",
-                           "parallelism": "host threads"},
+                "config": {"workload": workload(n, world), "parallelism": f"{cores} host threads",
+                           "sample": f"each step times a {n}x{rows} slab of the workload (same per-cell work)"},
                 "impl": "reference",
                 "cpu_baseline": {"value": r["value"], "unit": "Gcell-updates/s", "cores": cores,
                                  "kind": "port", "sample": r["sample"]},
@@ -269,12 +283,11 @@ def main():
             traffic = None
 
     line = {
-        "metric": "Gcell-updates/s (shallow-water step)", "value": round(value, 3), "unit": "Gcell-updates/s",
+        "metric": METRIC, "value": round(value, 3), "unit": "Gcell-updates/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic (Gaussian hump h=1+0.4exp(-r^2/(n/8)^2), hu=hv=0)",
-        "config": {"workload": f"shallow-water {n}x{n} {'fp32' if args.precision == 'f32' else 'fp64'}, reflective, "
-                               f"fixed dt=0.3*stable_dt (BASELINE config 3)",
+        "config": {"workload": workload(n, 1, args.precision),
                    "precision": args.precision, "diagnostics": args.diag,
                    "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else FAST_PARITY,
                    "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",

@@ -633,12 +633,13 @@ def bench_main(args, rank: int, world: int) -> int:
         from bench import BYTES_PER_CELL, peaks
         peak, src = peaks()
         per_gpu_gbs = BYTES_PER_CELL["f32"] * (cells / world) * args.steps / (total_ms / 1e3) / 1e9
-        line = {"metric": "Gcell-updates/s (shallow-water step)", "value": round(value, 3),
+        from bench import METRIC, workload
+        line = {"metric": METRIC, "value": round(value, 3),
                 "unit": "Gcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
-                "config": {"workload": f"shallow-water {n}x{n} fp32 per GPU, 2-D decomposed {px}x{py}, "
-                                       "one-cell halo exchange per step " +
+                "config": {"workload": workload(n, world),
+                           "exchange": "one-cell halo exchange per step " +
                                        ("fused into the step kernel (NVLink peer stores + mailbox flags)"
                                         if args.transport == "peer" else "(pack + NCCL send/recv + unpack)"),
                            "transport": args.transport,
