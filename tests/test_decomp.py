@@ -294,3 +294,37 @@ def test_local_fused_generic_kernel(precision):
     for f in ("H", "U", "V"):
         got = gather_interior(grid, [getattr(s, f).to_numpy()[1:-1, 1:-1] for s in states])
         assert np.array_equal(got, getattr(ref, f).to_numpy()[1:-1, 1:-1]), f
+
+
+_WATCHDOG_SCRIPT = r"""
+import ctypes, sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1107_2157_b200 import _native as N, swdemo
+from paper_1107_2157_b200.decomp import Mailbox, fill_sync, LEFT
+cfg = swdemo.SWConfig(nx=int(sys.argv[2]), ny=64, dt=0.05, variant=sys.argv[3])
+a = swdemo.init_state(cfg)
+b = swdemo.SWState(a.H.empty_like(), a.U.empty_like(), a.V.empty_like())
+mail, other = Mailbox(a.H.storage.device), Mailbox(a.H.storage.device)
+args = swdemo._step_args(a, b, 0.05, ("none", "reflective", "reflective", "reflective"), "fast", cfg.variant)
+fill_sync(args.sync, mail, {LEFT: other.word(1)}, 1)     # wait for epoch 1: nobody ever signals
+N.check(N.lib().fkc_sw_step(ctypes.byref(args), torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+print("UNEXPECTED: step completed")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["tma", "generic"])
+def test_missing_neighbour_fails_loudly(variant):
+    """A neighbour that never signals its mailbox must not hang the GPU: the
+    waiting warps trip the watchdog (~2 s) and trap, the process sees a CUDA
+    error and exits non-zero."""
+    import subprocess
+    import sys
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    t0 = time.time()
+    r = subprocess.run([sys.executable, "-c", _WATCHDOG_SCRIPT, root, "480", variant], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode != 0 and "UNEXPECTED" not in r.stdout, (r.stdout, r.stderr[-2000:])
+    assert time.time() - t0 < 100
