@@ -198,9 +198,10 @@ def main():
     ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
     ap.add_argument("--alt", type=int, default=1, choices=[0, 1],
                     help="TMA kernel: odd segments sweep top-down (L2 reuse of shared halo rows)")
-    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+    ap.add_argument("--transport", default="auto", choices=["auto", "peer", "nccl"],
                     help="N>1 halo exchange: peer = fused into the step kernel over NVLink peer memory "
-                         "(CUDA IPC + mailbox flags); nccl = pack + NCCL send/recv + unpack (baseline)")
+                         "(CUDA IPC + mailbox flags); nccl = pack + NCCL send/recv + unpack (baseline); "
+                         "auto = peer, falling back to nccl on every rank if the IPC setup fails")
     ap.add_argument("--diag", default="none", choices=["none", "diag", "cfl"],
                     help="fused reductions in the timed steps: none; diag = mass, max|hu|, max|hv|, error word "
                          "(run()'s per-step diagnostics); cfl = diag + the CFL bound, dt recomputed on device "

@@ -338,6 +338,10 @@ def initial_peer_exchange(grid: CartGrid, rank: int, st, lines: Dict[int, "N.Pee
                 N.check(L.fkc_copy2d(line.p[f] + line.stride * it, line.stride * it, src, p * it, it, t.ny, sp))
 
 
+class PeerSetupError(RuntimeError):
+    """CUDA-IPC peer setup failed on some rank (raised on every rank)."""
+
+
 class PeerExchange:
     """Fused exchange between the processes of a decomposed run (one per
     GPU): every rank exports its two state buffers (H,U,V of each parity) and
@@ -350,27 +354,46 @@ class PeerExchange:
         self.grid, self.rank = grid, rank
         dev = bufs[0].H.storage.device
         self.mail = Mailbox(dev)
-        mine = {"bufs": [[N.ipc_export(p) for p in _field_ptrs(b)] for b in bufs],
-                "mail": N.ipc_export(self.mail.ptr),
-                "pitch": bufs[0].H.pitch, "itemsize": bufs[0].H.storage.element_size()}
-        everyone = [None] * dist.get_world_size(group)
-        dist.all_gather_object(everyone, mine, group=group)
         self._opened: Dict[bytes, int] = {}
+        world = dist.get_world_size(group)
+        # every failure is agreed on collectively, so all ranks raise together
+        # (PeerSetupError) and a caller can fall back to another transport
+        try:
+            mine, err = {"bufs": [[N.ipc_export(p) for p in _field_ptrs(b)] for b in bufs],
+                         "mail": N.ipc_export(self.mail.ptr),
+                         "pitch": bufs[0].H.pitch, "itemsize": bufs[0].H.storage.element_size()}, None
+        except Exception as e:  # noqa: BLE001 - reported collectively
+            mine, err = None, f"rank {rank} export: {e}"
+        everyone = [None] * world
+        dist.all_gather_object(everyone, {"info": mine, "err": err}, group=group)
+        errs = [e["err"] for e in everyone if e["err"]]
+        if errs:
+            raise PeerSetupError("; ".join(errs))
         self.nbr = {s: grid.neighbor(rank, s) for s in (LEFT, RIGHT, DOWN, UP)}
         self.nbr = {s: n for s, n in self.nbr.items() if n is not None}
         # lines[p][side]: targets for a step whose OUTPUT parity is p
         self.lines = [{}, {}]
         self.signal: Dict[int, int] = {}
-        for s, n in self.nbr.items():
-            info = everyone[n]
-            nt = grid.tile(n)
-            for p in (0, 1):
-                ptrs = [self._open(h) + off for h, off in info["bufs"][p]]
-                line = N.PeerLine()
-                set_peer_line(line, s, ptrs, info["pitch"], nt.nx, nt.ny, info["itemsize"])
-                self.lines[p][s] = line
-            h, off = info["mail"]
-            self.signal[s] = self._open(h) + off + 4 * OPPOSITE[s]
+        err = None
+        try:
+            for s, n in self.nbr.items():
+                info = everyone[n]["info"]
+                nt = grid.tile(n)
+                for p in (0, 1):
+                    ptrs = [self._open(h) + off for h, off in info["bufs"][p]]
+                    line = N.PeerLine()
+                    set_peer_line(line, s, ptrs, info["pitch"], nt.nx, nt.ny, info["itemsize"])
+                    self.lines[p][s] = line
+                h, off = info["mail"]
+                self.signal[s] = self._open(h) + off + 4 * OPPOSITE[s]
+        except Exception as e:  # noqa: BLE001 - reported collectively
+            err = f"rank {rank} open: {e}"
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        errs = [e for e in errs if e]
+        if errs:
+            self.close()
+            raise PeerSetupError("; ".join(errs))
 
     def _open(self, handle: bytes) -> int:
         if handle not in self._opened:
@@ -419,8 +442,9 @@ class DistributedSimulation:
         import torch.distributed as dist
         from . import swdemo
         from .field import DeviceField, Field
-        if transport not in ("peer", "nccl"):
+        if transport not in ("peer", "nccl", "auto"):
             raise ValueError(f"unknown transport {transport!r}")
+        self.fallback_reason = None
         self.transport = transport
         self.cfg, self.grid, self.rank = cfg, grid, rank
         self.tile = grid.tile(rank)
@@ -445,7 +469,18 @@ class DistributedSimulation:
                                     tdt)
             self.ex.exchange(self.a)
         else:
-            self.peer = PeerExchange(grid, rank, (self.a, self.b), group)
+            try:
+                self.peer = PeerExchange(grid, rank, (self.a, self.b), group)
+            except PeerSetupError as e:
+                if transport == "peer":
+                    raise
+                # auto: every rank got the same error -> all fall back together
+                self.transport, self.fallback_reason = "nccl", str(e)
+                self.ex = HaloExchanger(grid, rank, DistTransport(group), NativeLines(stream),
+                                        st.H.storage.device, tdt)
+                self.ex.exchange(self.a)
+        if self.peer is not None:
+            self.transport = "peer"
             initial_peer_exchange(grid, rank, self.a, self.peer.lines[0], stream)
             (stream or torch.cuda.current_stream()).synchronize()
             dist.barrier(group)
@@ -641,13 +676,16 @@ def bench_main(args, rank: int, world: int) -> int:
                 "config": {"workload": workload(n, world),
                            "exchange": "one-cell halo exchange per step " +
                                        ("fused into the step kernel (NVLink peer stores + mailbox flags)"
-                                        if args.transport == "peer" else "(pack + NCCL send/recv + unpack)"),
-                           "transport": args.transport,
+                                        if sim.transport == "peer" else "(pack + NCCL send/recv + unpack)"),
+
                            "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
                 "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
                              "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
                 "gpu_launches": args.steps * sim._launches_per_step()}
+        line["config"]["transport"] = sim.transport
+        if sim.fallback_reason:
+            line["config"]["transport_fallback"] = sim.fallback_reason[:300]
         print(json.dumps(line))
     sim.close()
     dist.destroy_process_group()

@@ -328,3 +328,52 @@ def test_missing_neighbour_fails_loudly(variant):
                        text=True, timeout=120)
     assert r.returncode != 0 and "UNEXPECTED" not in r.stdout, (r.stdout, r.stderr[-2000:])
     assert time.time() - t0 < 100
+
+
+def _peer_error_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1107_2157_b200.decomp import CartGrid, PeerExchange, PeerSetupError
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        class F:
+            def __init__(self):
+                self.storage = torch.zeros(64)
+                self.pitch = 8
+
+            @property
+            def ptr(self):      # host memory: CUDA IPC export must fail
+                return self.storage.data_ptr()
+
+        class S:
+            def __init__(self):
+                self.H, self.U, self.V = F(), F(), F()
+        try:
+            PeerExchange(CartGrid(1, world, 8, 8), rank, (S(), S()))
+            q.put((rank, "no error"))
+        except PeerSetupError as e:
+            q.put((rank, "PeerSetupError" + (" with rank 0 and 1" if "rank 0" in str(e) and "rank 1" in str(e)
+                                              else "")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_setup_error_is_collective():
+    """CPU tier: when CUDA-IPC setup fails, every rank raises PeerSetupError
+    (agreed over the process group), so 'auto' falls back consistently
+    instead of leaving ranks stuck in a collective."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_error_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: "PeerSetupError with rank 0 and 1", 1: "PeerSetupError with rank 0 and 1"}, got
