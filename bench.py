@@ -384,7 +384,8 @@ def e2e_run(n, dt, args, dev):
             "h2d_bytes_per_step": round(state_bytes / steps, 1),
             "d2h_bytes_per_step": round((state_bytes + 40 * (steps + 1)) / steps, 1),
             "steps": steps, "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
-            "diagnostics": "per-step mass/max|hu|/max|hv| fused in the step kernel",
+            "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel, each step's "
+                           "40-byte row copied device->host after the step",
             "final_mass": res.rows[-1][3]}
 
 

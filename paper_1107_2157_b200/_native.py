@@ -79,7 +79,7 @@ class LoopArgs(ctypes.Structure):
     """fkc_sw_loop_args: the native time loop (fkc_sw_advance_n)."""
     _fields_ = [("step", StepArgs), ("first_step", ctypes.c_int64), ("steps", ctypes.c_int64),
                 ("slots", ctypes.c_void_p), ("dt_from_slots", ctypes.c_int32), ("want_cfl", ctypes.c_int32),
-                ("use_graph", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("use_graph", ctypes.c_int32), ("_pad", ctypes.c_int32), ("host_slots", ctypes.c_void_p)]
 
 
 _lib = None

@@ -359,6 +359,11 @@ static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
             a.dt_bound = L->dt_from_slots ? in + 3 : nullptr;
         }
         if (int rc = fkc_sw_step(&a, st)) return rc;
+        if (L->slots && L->host_slots) {
+            cudaError_t e = cudaMemcpyAsync(L->host_slots + 5 * (i + 1), L->slots + 5 * (i + 1), 5 * sizeof(uint64_t),
+                                            cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (diagnostics row): %s", cudaGetErrorString(e));
+        }
     }
     return FKC_OK;
 }

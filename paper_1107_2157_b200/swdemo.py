@@ -340,7 +340,7 @@ class Simulation:
     """
 
     def __init__(self, cfg: SWConfig, state: Optional[SWState] = None, diagnostics: bool = True,
-                 capacity: Optional[int] = None, stream=None, boundary=None):
+                 capacity: Optional[int] = None, stream=None, boundary=None, stream_rows: bool = False):
         torch = _torch()
         self.cfg = cfg
         self.stream = stream
@@ -353,11 +353,17 @@ class Simulation:
         self.n = 0
         cap = (capacity if capacity is not None else cfg.steps) + 1
         self.slots = ReductionSlots(cap, st.H.storage.device) if self.diag else None
+        # stream_rows: every step's diagnostics row is copied back into pinned
+        # host memory right after the step (stream-ordered, no host sync)
+        self.host_rows = None
         if self.diag:
             red = self.slots.reduce_struct(0)
             g = _grid(st.H)
             N.check(N.lib().fkc_sw_reduce_state(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, st.dx, st.dy,
                                                 st.g, ctypes.byref(red), _stream_ptr(stream)))
+            if stream_rows:
+                self.host_rows = torch.zeros((cap, 5), dtype=torch.int64, pin_memory=True)
+                self.host_rows[0:1].copy_(self.slots.buf[0:1], non_blocking=True)
         self._args = [None, None]
         self.torch = torch
 
@@ -375,6 +381,8 @@ class Simulation:
             L.slots = self.slots.buf.data_ptr()
             L.dt_from_slots = int(cfg.dt is None)
             L.want_cfl = int(cfg.dt is None)
+            if self.host_rows is not None:
+                L.host_slots = self.host_rows.data_ptr()
         L.use_graph = int(use_graph)
         return L
 
@@ -419,9 +427,14 @@ class Simulation:
         return s
 
     def diagnostics(self) -> dict:
-        """One device->host copy of all reduction slots so far."""
+        """All reduction rows so far: from the pinned host mirror the steps
+        streamed back (stream_rows=True), else one device->host copy."""
         if not self.diag:
             return {}
+        if self.host_rows is not None:
+            torch = self.torch
+            (self.stream if self.stream is not None else torch.cuda.current_stream()).synchronize()
+            return ReductionSlots.decode(self.host_rows[: self.n + 1].numpy())
         return ReductionSlots.decode(self.slots.buf[: self.n + 1].cpu().numpy())
 
     def rows(self) -> RunResult:
@@ -451,15 +464,17 @@ def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
     """Time loop: apply_boundary -> dt -> advance -> swap ->
     diagnostics (mass, max|hu|, max|hv|, dt), aborting on non-finite values.
 
-    The whole loop is enqueued on the GPU; per-step diagnostics come from the
-    reductions fused into each step and are read back once at the end.
+    The whole loop is enqueued on the GPU by one native call; per-step
+    diagnostics come from the reductions fused into each step and each
+    step's row is copied back to pinned host memory as soon as the step is
+    done (stream-ordered, no host synchronisation until the end).
     A host ``state`` is uploaded first; ``to_host=True`` returns the final
     state as host Fields (written into ``out``'s arrays when given).
     """
     if engine not in ENGINES:
         raise ValueError(f"engine {engine!r} is not provided by the B200 package "
                          f"(available: {ENGINES}); the CPU engines live in the reference")
-    sim = Simulation(cfg, state=state, diagnostics=True)
+    sim = Simulation(cfg, state=state, diagnostics=True, stream_rows=True)
     sim.advance(cfg.steps)
     res = sim.rows()
     if to_host or out is not None:

@@ -91,9 +91,9 @@ def test_struct_layout_matches_header():
       printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_peer_line), sizeof(fkc_sync),
              offsetof(fkc_sw_step_args, peer), offsetof(fkc_sw_step_args, sync),
              offsetof(fkc_sync, counter), offsetof(fkc_sync, epoch));
-      printf("%zu %zu %zu %zu %zu\n", sizeof(fkc_sw_loop_args), offsetof(fkc_sw_loop_args, first_step),
+      printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_sw_loop_args), offsetof(fkc_sw_loop_args, first_step),
              offsetof(fkc_sw_loop_args, slots), offsetof(fkc_sw_loop_args, want_cfl),
-             offsetof(fkc_sw_loop_args, use_graph));
+             offsetof(fkc_sw_loop_args, use_graph), offsetof(fkc_sw_loop_args, host_slots));
       return 0;
     }
     """
@@ -110,7 +110,7 @@ def test_struct_layout_matches_header():
             ctypes.sizeof(N.PeerLine), ctypes.sizeof(N.Sync), S.peer.offset, S.sync.offset,
             N.Sync.counter.offset, N.Sync.epoch.offset,
             ctypes.sizeof(N.LoopArgs), N.LoopArgs.first_step.offset, N.LoopArgs.slots.offset,
-            N.LoopArgs.want_cfl.offset, N.LoopArgs.use_graph.offset]
+            N.LoopArgs.want_cfl.offset, N.LoopArgs.use_graph.offset, N.LoopArgs.host_slots.offset]
     assert got == want
 
 
