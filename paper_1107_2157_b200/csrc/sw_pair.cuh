@@ -204,4 +204,155 @@ struct PairEngine {
     }
 };
 
+// ---------------------------------------------------------------------------
+// ExactPairEngine: f32 exact mode with the MULTIPLIES (and the FMAs of the
+// exact division) on the packed pipe.  The additions stay scalar __fadd_rn:
+// ptxas 12.9 contracts an f32x2 multiply feeding an f32x2 add into FFMA2 even
+// with explicit .rn and -fmad=false, which would break the node-by-node
+// order; an FMUL2 feeding scalar adds is left alone.  Every node is still
+// one IEEE RN operation in the wave_advance.fk order (sw_math.cuh cell_q /
+// y_face / update_cell), so the results are bit-identical (tested).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 sadd2(float2 a, float2 b) {
+    return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 ssub2(float2 a, float2 b) {
+    return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 pmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+// RN(a[i] / b) per element: DIV_GUARD (shared refined reciprocal, residual
+// and correction on the packed pipe, scalar range guard) or DIV_FIXUP
+// (scalar, never fails) -- the sequences of sw_math.cuh div_group.
+template <int DM, int N>
+__device__ __forceinline__ void div2(float2 b, const float2 (&a)[N], float2 (&q)[N], bool& ok) {
+    if constexpr (DM == DIV_GUARD) {
+        const float2 r0 = rcp2(b);
+        const float2 r = __ffma2_rn(r0, __ffma2_rn(make_float2(-b.x, -b.y), r0, bc2(1.0f)), r0);
+        const float2 nr = make_float2(-r.x, -r.y);
+        bool g = (b.x >= 0x1p-24f) & (b.x <= 0x1p+24f) & (b.y >= 0x1p-24f) & (b.y <= 0x1p+24f);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float2 qi = pmul2(a[i], r);
+            const float2 res = __ffma2_rn(b, qi, make_float2(-a[i].x, -a[i].y));
+            q[i] = __ffma2_rn(nr, res, qi);
+            const float ax = fabsf(a[i].x), ay = fabsf(a[i].y);
+            g = g & ((ax >= 0x1p-100f) | (a[i].x == 0.0f)) & (ax <= 0x1p+100f) &
+                ((ay >= 0x1p-100f) | (a[i].y == 0.0f)) & (ay <= 0x1p+100f);
+        }
+        ok = ok & g;
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float ax[1] = {a[i].x}, ay[1] = {a[i].y};
+            float qx[1], qy[1];
+            div_group<float, DM, 1>(b.x, ax, qx, ok);
+            div_group<float, DM, 1>(b.y, ay, qy, ok);
+            q[i] = make_float2(qx[0], qy[0]);
+        }
+    }
+}
+
+template <int DM>
+__device__ __forceinline__ CellQ2 cell_q2_exact(float2 h, float2 u, float2 v, const Coef2& c, bool& ok) {
+    CellQ2 q;
+    q.h = h; q.u = u; q.v = v;
+    const float2 num[3] = {pmul2(u, u), pmul2(v, v), pmul2(u, v)};
+    float2 quo[3];
+    div2<DM, 3>(h, num, quo, ok);
+    const float2 gh2 = pmul2(pmul2(c.g2, h), h);
+    q.fu = sadd2(quo[0], gh2);
+    q.fv = sadd2(quo[1], gh2);
+    q.cr = quo[2];
+    return q;
+}
+
+template <int DM>
+__device__ __forceinline__ FaceF2 y_face2_exact(const CellQ2& D, const CellQ2& U, const Coef2& c, bool& ok) {
+    const float2 Hy = sadd2(pmul2(c.half, sadd2(D.h, U.h)), pmul2(c.cy2, ssub2(D.v, U.v)));
+    const float2 Uy = sadd2(pmul2(c.half, sadd2(D.u, U.u)), pmul2(c.cy2, ssub2(D.cr, U.cr)));
+    const float2 Vy = sadd2(pmul2(c.half, sadd2(D.v, U.v)), pmul2(c.cy2, ssub2(D.fv, U.fv)));
+    const float2 num[2] = {pmul2(Uy, Vy), pmul2(Vy, Vy)};
+    float2 quo[2];
+    div2<DM, 2>(Hy, num, quo, ok);
+    FaceF2 f;
+    f.fh = Vy;
+    f.fu = quo[0];
+    f.fv = sadd2(quo[1], pmul2(pmul2(c.g2, Hy), Hy));
+    return f;
+}
+
+struct ExactPairEngine {
+    static constexpr int CPL = 4;
+    CellQ2 pc[2];
+    FaceF2 pdx[2], ydn[2];
+    CellQ2 nc[2];
+    FaceF2 ndx[2], yup[2];
+    Coef2 c2;
+
+    __device__ __forceinline__ void init(const Coef<float>& c) {
+        c2.half = bc2(c.half); c2.cx2 = bc2(c.cx2); c2.cy2 = bc2(c.cy2);
+        c2.cx = bc2(c.cx); c2.cy = bc2(c.cy); c2.g2 = bc2(c.g2);
+        const float2 one = bc2(1.f), zero = bc2(0.f);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            pc[j] = CellQ2{one, zero, zero, zero, zero, zero};
+            pdx[j] = ydn[j] = FaceF2{zero, zero, zero};
+        }
+    }
+
+    template <int DM>
+    __device__ __forceinline__ void row(const VecF<float>& h, const VecF<float>& u, const VecF<float>& v,
+                                        bool have_prev, bool want_x, const Coef<float>& c, bool& ok) {
+        nc[0] = cell_q2_exact<DM>(make_float2(h.v[0], h.v[1]), make_float2(u.v[0], u.v[1]),
+                                  make_float2(v.v[0], v.v[1]), c2, ok);
+        nc[1] = cell_q2_exact<DM>(make_float2(h.v[2], h.v[3]), make_float2(u.v[2], u.v[3]),
+                                  make_float2(v.v[2], v.v[3]), c2, ok);
+        if (have_prev) {
+            yup[0] = y_face2_exact<DM>(pc[0], nc[0], c2, ok);
+            yup[1] = y_face2_exact<DM>(pc[1], nc[1], c2, ok);
+        }
+        if (want_x) {
+            CellQ<float> nb;  // first cell of lane+1
+            nb.h = __shfl_down_sync(0xffffffffu, nc[0].h.x, 1);
+            nb.u = __shfl_down_sync(0xffffffffu, nc[0].u.x, 1);
+            nb.v = __shfl_down_sync(0xffffffffu, nc[0].v.x, 1);
+            nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu.x, 1);
+            nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr.x, 1);
+            nb.fv = 0.f;
+            const FaceF<float> f01 = x_face<float, DM>(nc[0].lo(), nc[0].hi(), c, ok);
+            const FaceF<float> f12 = x_face<float, DM>(nc[0].hi(), nc[1].lo(), c, ok);
+            const FaceF<float> f23 = x_face<float, DM>(nc[1].lo(), nc[1].hi(), c, ok);
+            const FaceF<float> f34 = x_face<float, DM>(nc[1].hi(), nb, c, ok);
+            FaceF<float> fl;
+            fl.fh = __shfl_up_sync(0xffffffffu, f34.fh, 1);
+            fl.fu = __shfl_up_sync(0xffffffffu, f34.fu, 1);
+            fl.fv = __shfl_up_sync(0xffffffffu, f34.fv, 1);
+            ndx[0].fh = make_float2(__fsub_rn(fl.fh, f01.fh), __fsub_rn(f01.fh, f12.fh));
+            ndx[0].fu = make_float2(__fsub_rn(fl.fu, f01.fu), __fsub_rn(f01.fu, f12.fu));
+            ndx[0].fv = make_float2(__fsub_rn(fl.fv, f01.fv), __fsub_rn(f01.fv, f12.fv));
+            ndx[1].fh = make_float2(__fsub_rn(f12.fh, f23.fh), __fsub_rn(f23.fh, f34.fh));
+            ndx[1].fu = make_float2(__fsub_rn(f12.fu, f23.fu), __fsub_rn(f23.fu, f34.fu));
+            ndx[1].fv = make_float2(__fsub_rn(f12.fv, f23.fv), __fsub_rn(f23.fv, f34.fv));
+        }
+    }
+    // q' = (q + cx*(F_left - F_right)) + cy*(G_down - G_up), RN per node
+    template <int DM>
+    __device__ __forceinline__ void update(const Coef<float>&, float (&oh)[4], float (&ou)[4], float (&ov)[4]) const {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float2 h = sadd2(sadd2(pc[j].h, pmul2(c2.cx, pdx[j].fh)), pmul2(c2.cy, ssub2(ydn[j].fh, yup[j].fh)));
+            const float2 u = sadd2(sadd2(pc[j].u, pmul2(c2.cx, pdx[j].fu)), pmul2(c2.cy, ssub2(ydn[j].fu, yup[j].fu)));
+            const float2 v = sadd2(sadd2(pc[j].v, pmul2(c2.cx, pdx[j].fv)), pmul2(c2.cy, ssub2(ydn[j].fv, yup[j].fv)));
+            oh[2 * j] = h.x; oh[2 * j + 1] = h.y;
+            ou[2 * j] = u.x; ou[2 * j + 1] = u.y;
+            ov[2 * j] = v.x; ov[2 * j + 1] = v.y;
+        }
+    }
+    __device__ __forceinline__ void shift() {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) { pc[j] = nc[j]; ydn[j] = yup[j]; pdx[j] = ndx[j]; }
+    }
+};
+
 }  // namespace fkc

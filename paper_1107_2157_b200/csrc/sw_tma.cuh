@@ -63,6 +63,9 @@ constexpr int THREADS = WARPS * 32;
 #ifndef FKC_TMA_PAIR
 #define FKC_TMA_PAIR 1        // f32 fast mode on the packed FP32 pipe (FFMA2 / FADD2 / FMUL2)
 #endif
+#ifndef FKC_TMA_EXACT_PAIR
+#define FKC_TMA_EXACT_PAIR 1  // f32 exact mode: multiplies / division FMAs on the packed pipe
+#endif
 #ifndef FKC_FAST_UNROLL
 #define FKC_FAST_UNROLL 2     // rows of a stage unrolled in fast mode (even: the register window renames)
 #endif
@@ -276,7 +279,10 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     // the y-sweep's register window: packed-pair engine for f32 fast mode
     // (sw_pair.cuh), scalar engine otherwise
     constexpr bool PAIR = FAST && sizeof(T) == 4 && FKC_TMA_PAIR;
-    using Engine = typename std::conditional<PAIR, PairEngine, ScalarEngine<T, CPL>>::type;
+    constexpr bool EXACT_PAIR = !FAST && sizeof(T) == 4 && FKC_TMA_EXACT_PAIR;
+    using Engine = typename std::conditional<
+        PAIR, PairEngine,
+        typename std::conditional<EXACT_PAIR, ExactPairEngine, ScalarEngine<T, CPL>>::type>::type;
     Engine eng;
     eng.init(c);
     // element offset of the row updated at loaded-row index n (lane's cell 0),
