@@ -282,6 +282,36 @@ __device__ __forceinline__ FaceF2 y_face2_exact(const CellQ2& D, const CellQ2& U
     return f;
 }
 
+// x-faces between the cells of L and R (two faces at once; statements Hx,
+// Ux, Vx).  The cell quantities only enter through scalar sums / differences,
+// so the pairs L and R never have to exist as register pairs.
+template <int DM>
+__device__ __forceinline__ FaceF2 x_face2_exact(const CellQ2& L, const CellQ2& R, const Coef2& c, bool& ok) {
+    const float2 Hx = sadd2(pmul2(c.half, sadd2(L.h, R.h)), pmul2(c.cx2, ssub2(L.u, R.u)));
+    const float2 Ux = sadd2(pmul2(c.half, sadd2(L.u, R.u)), pmul2(c.cx2, ssub2(L.fu, R.fu)));
+    const float2 Vx = sadd2(pmul2(c.half, sadd2(L.v, R.v)), pmul2(c.cx2, ssub2(L.cr, R.cr)));
+    const float2 num[2] = {pmul2(Ux, Ux), pmul2(Ux, Vx)};
+    float2 quo[2];
+    div2<DM, 2>(Hx, num, quo, ok);
+    FaceF2 f;
+    f.fh = Ux;
+    f.fu = sadd2(quo[0], pmul2(pmul2(c.g2, Hx), Hx));
+    f.fv = quo[1];
+    return f;
+}
+
+__device__ __forceinline__ CellQ2 cells2(const CellQ2& a, bool ahi, const CellQ2& b, bool bhi) {
+    auto pick = [](float2 p, bool hi) { return hi ? p.y : p.x; };
+    CellQ2 q;
+    q.h = make_float2(pick(a.h, ahi), pick(b.h, bhi));
+    q.u = make_float2(pick(a.u, ahi), pick(b.u, bhi));
+    q.v = make_float2(pick(a.v, ahi), pick(b.v, bhi));
+    q.fu = make_float2(pick(a.fu, ahi), pick(b.fu, bhi));
+    q.fv = make_float2(pick(a.fv, ahi), pick(b.fv, bhi));
+    q.cr = make_float2(pick(a.cr, ahi), pick(b.cr, bhi));
+    return q;
+}
+
 struct ExactPairEngine {
     static constexpr int CPL = 4;
     CellQ2 pc[2];
@@ -320,20 +350,24 @@ struct ExactPairEngine {
             nb.fu = __shfl_down_sync(0xffffffffu, nc[0].fu.x, 1);
             nb.cr = __shfl_down_sync(0xffffffffu, nc[0].cr.x, 1);
             nb.fv = 0.f;
-            const FaceF<float> f01 = x_face<float, DM>(nc[0].lo(), nc[0].hi(), c, ok);
-            const FaceF<float> f12 = x_face<float, DM>(nc[0].hi(), nc[1].lo(), c, ok);
-            const FaceF<float> f23 = x_face<float, DM>(nc[1].lo(), nc[1].hi(), c, ok);
-            const FaceF<float> f34 = x_face<float, DM>(nc[1].hi(), nb, c, ok);
-            FaceF<float> fl;
-            fl.fh = __shfl_up_sync(0xffffffffu, f34.fh, 1);
-            fl.fu = __shfl_up_sync(0xffffffffu, f34.fu, 1);
-            fl.fv = __shfl_up_sync(0xffffffffu, f34.fv, 1);
-            ndx[0].fh = make_float2(__fsub_rn(fl.fh, f01.fh), __fsub_rn(f01.fh, f12.fh));
-            ndx[0].fu = make_float2(__fsub_rn(fl.fu, f01.fu), __fsub_rn(f01.fu, f12.fu));
-            ndx[0].fv = make_float2(__fsub_rn(fl.fv, f01.fv), __fsub_rn(f01.fv, f12.fv));
-            ndx[1].fh = make_float2(__fsub_rn(f12.fh, f23.fh), __fsub_rn(f23.fh, f34.fh));
-            ndx[1].fu = make_float2(__fsub_rn(f12.fu, f23.fu), __fsub_rn(f23.fu, f34.fu));
-            ndx[1].fv = make_float2(__fsub_rn(f12.fv, f23.fv), __fsub_rn(f23.fv, f34.fv));
+            CellQ2 nbq;
+            nbq.h = bc2(nb.h); nbq.u = bc2(nb.u); nbq.v = bc2(nb.v); nbq.fu = bc2(nb.fu); nbq.fv = bc2(0.f);
+            nbq.cr = bc2(nb.cr);
+            // faces (f01, f23) = x_face((c0, c2), (c1, c3)); (f12, f34) = x_face((c1, c3), (c2, c4))
+            const FaceF2 F0 = x_face2_exact<DM>(cells2(nc[0], false, nc[1], false), cells2(nc[0], true, nc[1], true),
+                                                c2, ok);
+            const FaceF2 F1 = x_face2_exact<DM>(cells2(nc[0], true, nc[1], true), cells2(nc[1], false, nbq, false),
+                                                c2, ok);
+            FaceF<float> fl;  // face left of c0 = lane-1's f34
+            fl.fh = __shfl_up_sync(0xffffffffu, F1.fh.y, 1);
+            fl.fu = __shfl_up_sync(0xffffffffu, F1.fu.y, 1);
+            fl.fv = __shfl_up_sync(0xffffffffu, F1.fv.y, 1);
+            ndx[0].fh = make_float2(__fsub_rn(fl.fh, F0.fh.x), __fsub_rn(F0.fh.x, F1.fh.x));
+            ndx[0].fu = make_float2(__fsub_rn(fl.fu, F0.fu.x), __fsub_rn(F0.fu.x, F1.fu.x));
+            ndx[0].fv = make_float2(__fsub_rn(fl.fv, F0.fv.x), __fsub_rn(F0.fv.x, F1.fv.x));
+            ndx[1].fh = make_float2(__fsub_rn(F1.fh.x, F0.fh.y), __fsub_rn(F0.fh.y, F1.fh.y));
+            ndx[1].fu = make_float2(__fsub_rn(F1.fu.x, F0.fu.y), __fsub_rn(F0.fu.y, F1.fu.y));
+            ndx[1].fv = make_float2(__fsub_rn(F1.fv.x, F0.fv.y), __fsub_rn(F0.fv.y, F1.fv.y));
         }
     }
     // q' = (q + cx*(F_left - F_right)) + cy*(G_down - G_up), RN per node
