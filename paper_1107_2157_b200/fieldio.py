@@ -154,6 +154,28 @@ def write_config(path: str, cfg) -> None:
         fh.write("\n".join(lines) + "\n")
 
 
+def save_state_npz(path: str, state, rows=None) -> None:
+    """Checkpoint a state (host or device) to one .npz: H, U, V full arrays
+    plus g, dx, dy, t, precision and optionally the diagnostics rows
+    (checkpoint = state to host Fields)."""
+    host = state.to_host() if getattr(state, "on_device", False) else state
+    extra = {} if rows is None else {"rows": np.asarray(rows, np.float64).reshape(-1, len(DIAG_HEADER))}
+    np.savez(path, H=host.H.data, U=host.U.data, V=host.V.data,
+             meta=np.array([host.g, host.dx, host.dy, host.t], np.float64),
+             precision=np.array(host.H.precision), **extra)
+
+
+def load_state_npz(path: str):
+    """Inverse of save_state_npz: (host SWState, rows or None)."""
+    from .swdemo import SWState
+    d = np.load(path)
+    prec = str(d["precision"])
+    fields = [Field(Extent(d[k].shape[1], d[k].shape[0]), d[k].astype(dtype_of(prec)), prec) for k in "HUV"]
+    g, dx, dy, t = (float(x) for x in d["meta"])
+    rows = d["rows"] if "rows" in d.files else None
+    return SWState(*fields, g, dx, dy, t), rows
+
+
 def state_paths(run_dir: str) -> Dict[str, str]:
     return {"H": os.path.join(run_dir, "H.csv"), "U": os.path.join(run_dir, "U.csv"),
             "V": os.path.join(run_dir, "V.csv"), "diag": os.path.join(run_dir, "diagnostics.csv")}

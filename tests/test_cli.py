@@ -160,3 +160,17 @@ def test_cmd_bench_rows(tmp_path, capsys):
     for r in rows:
         e, w, k, ms, g = r.split(",")
         assert float(ms) > 0 and np.isfinite(float(ms)) and float(g) > 0
+
+
+def test_checkpoint_npz_roundtrip(tmp_path):
+    from paper_1107_2157_b200 import swdemo
+    H, U, V = so.random_state(20, 12, "f32", seed=8)
+    st = swdemo.SWState(*(Field.from_array(a, "f32") for a in (H, U, V)), 9.81, 0.5, 0.25, 3.5)
+    rows = [(1, 0.1, 0.1, 12.0, 0.01, 0.02), (2, 0.2, 0.1, 12.0, 0.011, 0.021)]
+    fn = str(tmp_path / "ck.npz")
+    fieldio.save_state_npz(fn, st, rows)
+    back, r = fieldio.load_state_npz(fn)
+    assert (back.g, back.dx, back.dy, back.t) == (9.81, 0.5, 0.25, 3.5)
+    for a, b in zip((back.H, back.U, back.V), (H, U, V)):
+        assert a.precision == "f32" and a.data.tobytes() == b.tobytes()
+    assert np.array_equal(r, np.array(rows))
