@@ -102,6 +102,7 @@ struct FaceF2 {
 };
 struct Coef2 {
     float2 half, cx2, cy2, cx, cy, g2;
+    bool absorb;   // g/2 >= 1/4: tiny fxu quotients are absorbed (ExactPairEngine)
 };
 
 // fxu(h,u) = u*u/h + g2*h*h, fxu(h,v), cross = u*v/h with one reciprocal
@@ -142,6 +143,7 @@ struct PairEngine {
     __device__ __forceinline__ void init(const Coef<float>& c) {
         c2.half = bc2(c.half); c2.cx2 = bc2(c.cx2); c2.cy2 = bc2(c.cy2);
         c2.cx = bc2(c.cx); c2.cy = bc2(c.cy); c2.g2 = bc2(c.g2);
+        c2.absorb = false;
         // benign window (a lake at rest): a branch-free first row computes
         // finite, discarded faces
         const float2 one = bc2(1.f), zero = bc2(0.f);
@@ -221,34 +223,65 @@ __device__ __forceinline__ float2 ssub2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 pmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
-// RN(a[i] / b) per element: DIV_GUARD (shared refined reciprocal, residual
-// and correction on the packed pipe, scalar range guard) or DIV_FIXUP
-// (scalar, never fails) -- the sequences of sw_math.cuh div_group.
-template <int DM, int N>
-__device__ __forceinline__ void div2(float2 b, const float2 (&a)[N], float2 (&q)[N], bool& ok) {
+// RN(a / b) per element for the numerators over one denominator pair b, in
+// two classes (sequences and fallbacks of sw_math.cuh div_group):
+//  * af: fxu numerators (q^2, the quotient is added to g/2 h^2).  With
+//    `absorb` (g/2 >= 1/4) a tiny |a| < 2^-100 needs no exactness: for
+//    b >= 2^-24 the quotient is < 2^-76 while half an ulp of g/2 b^2 >=
+//    2^-50 is >= 2^-74, so RN(q + g/2 b^2) = g/2 b^2 for the oracle's q and
+//    ours alike -- the lean sequence suffices.
+//  * ac: cross numerators (u v, added to values of their own magnitude).
+//    Always scaled by 2^64 (exact), divided in the normal range and scaled
+//    back (exact whenever the quotient is normal); so tiny-but-normal
+//    quotients -- the far field of a wave -- need no fixup.
+// DIV_GUARD clears ok when an operand is outside that (b outside
+// [2^-24, 2^24], |a| too large, a subnormal cross quotient, inf / nan);
+// DIV_FIXUP is the scalar never-failing path for such rows.
+template <int DM, int NF, int NC>
+__device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const float2 (&ac)[NC], float2 (&qf)[NF],
+                                     float2 (&qc)[NC], bool absorb, bool& ok) {
     if constexpr (DM == DIV_GUARD) {
         const float2 r0 = rcp2(b);
         const float2 r = __ffma2_rn(r0, __ffma2_rn(make_float2(-b.x, -b.y), r0, bc2(1.0f)), r0);
         const float2 nr = make_float2(-r.x, -r.y);
         bool g = (b.x >= 0x1p-24f) & (b.x <= 0x1p+24f) & (b.y >= 0x1p-24f) & (b.y <= 0x1p+24f);
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const float2 qi = pmul2(a[i], r);
-            const float2 res = __ffma2_rn(b, qi, make_float2(-a[i].x, -a[i].y));
-            q[i] = __ffma2_rn(nr, res, qi);
-            const float ax = fabsf(a[i].x), ay = fabsf(a[i].y);
-            g = g & ((ax >= 0x1p-100f) | (a[i].x == 0.0f)) & (ax <= 0x1p+100f) &
-                ((ay >= 0x1p-100f) | (a[i].y == 0.0f)) & (ay <= 0x1p+100f);
+        for (int i = 0; i < NF; ++i) {
+            const float2 qi = pmul2(af[i], r);
+            const float2 res = __ffma2_rn(b, qi, make_float2(-af[i].x, -af[i].y));
+            qf[i] = __ffma2_rn(nr, res, qi);
+            const float ax = fabsf(af[i].x), ay = fabsf(af[i].y);
+            g = g & ((ax >= 0x1p-100f) | (af[i].x == 0.0f) | absorb) & (ax <= 0x1p+100f) &
+                ((ay >= 0x1p-100f) | (af[i].y == 0.0f) | absorb) & (ay <= 0x1p+100f);
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+            const float2 as = pmul2(ac[i], bc2(0x1p64f));
+            const float2 qi = pmul2(as, r);
+            const float2 res = __ffma2_rn(b, qi, make_float2(-as.x, -as.y));
+            const float2 qs = __ffma2_rn(nr, res, qi);
+            qc[i] = pmul2(qs, bc2(0x1p-64f));
+            const float sx = fabsf(qs.x), sy = fabsf(qs.y);
+            g = g & (fabsf(ac[i].x) <= 0x1p+36f) & (fabsf(ac[i].y) <= 0x1p+36f) &
+                ((sx >= 0x1p-62f) | (qs.x == 0.0f)) & ((sy >= 0x1p-62f) | (qs.y == 0.0f));
         }
         ok = ok & g;
     } else {
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const float ax[1] = {a[i].x}, ay[1] = {a[i].y};
+        for (int i = 0; i < NF; ++i) {
+            const float ax[1] = {af[i].x}, ay[1] = {af[i].y};
             float qx[1], qy[1];
             div_group<float, DM, 1>(b.x, ax, qx, ok);
             div_group<float, DM, 1>(b.y, ay, qy, ok);
-            q[i] = make_float2(qx[0], qy[0]);
+            qf[i] = make_float2(qx[0], qy[0]);
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+            const float ax[1] = {ac[i].x}, ay[1] = {ac[i].y};
+            float qx[1], qy[1];
+            div_group<float, DM, 1>(b.x, ax, qx, ok);
+            div_group<float, DM, 1>(b.y, ay, qy, ok);
+            qc[i] = make_float2(qx[0], qy[0]);
         }
     }
 }
@@ -257,13 +290,13 @@ template <int DM>
 __device__ __forceinline__ CellQ2 cell_q2_exact(float2 h, float2 u, float2 v, const Coef2& c, bool& ok) {
     CellQ2 q;
     q.h = h; q.u = u; q.v = v;
-    const float2 num[3] = {pmul2(u, u), pmul2(v, v), pmul2(u, v)};
-    float2 quo[3];
-    div2<DM, 3>(h, num, quo, ok);
+    const float2 nf[2] = {pmul2(u, u), pmul2(v, v)}, nc[1] = {pmul2(u, v)};
+    float2 qf[2], qc[1];
+    div2<DM, 2, 1>(h, nf, nc, qf, qc, c.absorb, ok);
     const float2 gh2 = pmul2(pmul2(c.g2, h), h);
-    q.fu = sadd2(quo[0], gh2);
-    q.fv = sadd2(quo[1], gh2);
-    q.cr = quo[2];
+    q.fu = sadd2(qf[0], gh2);
+    q.fv = sadd2(qf[1], gh2);
+    q.cr = qc[0];
     return q;
 }
 
@@ -272,13 +305,13 @@ __device__ __forceinline__ FaceF2 y_face2_exact(const CellQ2& D, const CellQ2& U
     const float2 Hy = sadd2(pmul2(c.half, sadd2(D.h, U.h)), pmul2(c.cy2, ssub2(D.v, U.v)));
     const float2 Uy = sadd2(pmul2(c.half, sadd2(D.u, U.u)), pmul2(c.cy2, ssub2(D.cr, U.cr)));
     const float2 Vy = sadd2(pmul2(c.half, sadd2(D.v, U.v)), pmul2(c.cy2, ssub2(D.fv, U.fv)));
-    const float2 num[2] = {pmul2(Uy, Vy), pmul2(Vy, Vy)};
-    float2 quo[2];
-    div2<DM, 2>(Hy, num, quo, ok);
+    const float2 nf[1] = {pmul2(Vy, Vy)}, nc[1] = {pmul2(Uy, Vy)};
+    float2 qf[1], qc[1];
+    div2<DM, 1, 1>(Hy, nf, nc, qf, qc, c.absorb, ok);
     FaceF2 f;
     f.fh = Vy;
-    f.fu = quo[0];
-    f.fv = sadd2(quo[1], pmul2(pmul2(c.g2, Hy), Hy));
+    f.fu = qc[0];
+    f.fv = sadd2(qf[0], pmul2(pmul2(c.g2, Hy), Hy));
     return f;
 }
 
@@ -290,13 +323,13 @@ __device__ __forceinline__ FaceF2 x_face2_exact(const CellQ2& L, const CellQ2& R
     const float2 Hx = sadd2(pmul2(c.half, sadd2(L.h, R.h)), pmul2(c.cx2, ssub2(L.u, R.u)));
     const float2 Ux = sadd2(pmul2(c.half, sadd2(L.u, R.u)), pmul2(c.cx2, ssub2(L.fu, R.fu)));
     const float2 Vx = sadd2(pmul2(c.half, sadd2(L.v, R.v)), pmul2(c.cx2, ssub2(L.cr, R.cr)));
-    const float2 num[2] = {pmul2(Ux, Ux), pmul2(Ux, Vx)};
-    float2 quo[2];
-    div2<DM, 2>(Hx, num, quo, ok);
+    const float2 nf[1] = {pmul2(Ux, Ux)}, nc[1] = {pmul2(Ux, Vx)};
+    float2 qf[1], qc[1];
+    div2<DM, 1, 1>(Hx, nf, nc, qf, qc, c.absorb, ok);
     FaceF2 f;
     f.fh = Ux;
-    f.fu = sadd2(quo[0], pmul2(pmul2(c.g2, Hx), Hx));
-    f.fv = quo[1];
+    f.fu = sadd2(qf[0], pmul2(pmul2(c.g2, Hx), Hx));
+    f.fv = qc[0];
     return f;
 }
 
@@ -323,6 +356,7 @@ struct ExactPairEngine {
     __device__ __forceinline__ void init(const Coef<float>& c) {
         c2.half = bc2(c.half); c2.cx2 = bc2(c.cx2); c2.cy2 = bc2(c.cy2);
         c2.cx = bc2(c.cx); c2.cy = bc2(c.cy); c2.g2 = bc2(c.g2);
+        c2.absorb = c.g2 >= 0.25f;
         const float2 one = bc2(1.f), zero = bc2(0.f);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
