@@ -233,9 +233,11 @@ __device__ __forceinline__ float2 pmul2(float2 a, float2 b) { return __fmul2_rn(
 //  * ac: cross numerators (u v, added to values of their own magnitude).
 //    Always scaled by 2^64 (exact), divided in the normal range and scaled
 //    back (exact whenever the quotient is normal); so tiny-but-normal
-//    quotients -- the far field of a wave -- need no fixup.
+//    quotients -- the far field of a wave -- need no fixup, and a subnormal
+//    quotient is redone for that element alone in closed form
+//    (fdiv_subnormal_rn).
 // DIV_GUARD clears ok when an operand is outside that (b outside
-// [2^-24, 2^24], |a| too large, a subnormal cross quotient, inf / nan);
+// [2^-24, 2^24], |a| too large, inf / nan);
 // DIV_FIXUP is the scalar never-failing path for such rows.
 template <int DM, int NF, int NC>
 __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const float2 (&ac)[NC], float2 (&qf)[NF],
@@ -261,9 +263,12 @@ __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const flo
             const float2 res = __ffma2_rn(b, qi, make_float2(-as.x, -as.y));
             const float2 qs = __ffma2_rn(nr, res, qi);
             qc[i] = pmul2(qs, bc2(0x1p-64f));
+            // a subnormal quotient (|qs| < 2^-62): that element alone takes the
+            // closed-form exact path (divergent, sparse) instead of failing the row
             const float sx = fabsf(qs.x), sy = fabsf(qs.y);
-            g = g & (fabsf(ac[i].x) <= 0x1p+36f) & (fabsf(ac[i].y) <= 0x1p+36f) &
-                ((sx >= 0x1p-62f) | (qs.x == 0.0f)) & ((sy >= 0x1p-62f) | (qs.y == 0.0f));
+            if ((sx < 0x1p-62f) & (qs.x != 0.0f)) qc[i].x = fdiv_subnormal_rn(ac[i].x, b.x);
+            if ((sy < 0x1p-62f) & (qs.y != 0.0f)) qc[i].y = fdiv_subnormal_rn(ac[i].y, b.y);
+            g = g & (fabsf(ac[i].x) <= 0x1p+36f) & (fabsf(ac[i].y) <= 0x1p+36f);
         }
         ok = ok & g;
     } else {

@@ -69,6 +69,9 @@ constexpr int THREADS = WARPS * 32;
 #ifndef FKC_FAST_UNROLL
 #define FKC_FAST_UNROLL 2     // rows of a stage unrolled in fast mode (even: the register window renames)
 #endif
+#ifndef FKC_FIX_PERSIST
+#define FKC_FIX_PERSIST 0     // exact mode: rows that stay on the fixup variant after a guard failure
+#endif
 #ifndef FKC_EXACT_UNROLL
 #define FKC_EXACT_UNROLL 1
 #endif
@@ -341,13 +344,13 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 if (!fix_mode && !FKC_EXACT_ALWAYS_FIXUP) {
                     eng.template row<DIV_GUARD>(hv, uv, vv, have_prev, want_x, c, ok);
                     if (__any_sync(0xffffffffu, !ok)) {
-                        fix_mode = true;
+                        fix_mode = FKC_FIX_PERSIST > 0;
                         fix_rows = 0;
                         eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
                     }
                 } else {
                     eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
-                    if (++fix_rows >= 16) fix_mode = false;
+                    if (++fix_rows >= FKC_FIX_PERSIST) fix_mode = false;
                 }
             }
             // full-step update of the previous row (row y0 + n - 2; top-down: ytop - n + 1)
