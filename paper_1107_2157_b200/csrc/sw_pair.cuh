@@ -253,8 +253,9 @@ __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const flo
             const float2 res = __ffma2_rn(b, qi, make_float2(-af[i].x, -af[i].y));
             qf[i] = __ffma2_rn(nr, res, qi);
             const float ax = fabsf(af[i].x), ay = fabsf(af[i].y);
-            g = g & ((ax >= 0x1p-100f) | (af[i].x == 0.0f) | absorb) & (ax <= 0x1p+100f) &
-                ((ay >= 0x1p-100f) | (af[i].y == 0.0f) | absorb) & (ay <= 0x1p+100f);
+            g = g & (ax <= 0x1p+100f) & (ay <= 0x1p+100f);
+            if (!absorb)   // warp-uniform
+                g = g & ((ax >= 0x1p-100f) | (af[i].x == 0.0f)) & ((ay >= 0x1p-100f) | (af[i].y == 0.0f));
         }
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
@@ -265,9 +266,12 @@ __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const flo
             qc[i] = pmul2(qs, bc2(0x1p-64f));
             // a subnormal quotient (|qs| < 2^-62): that element alone takes the
             // closed-form exact path (divergent, sparse) instead of failing the row
-            const float sx = fabsf(qs.x), sy = fabsf(qs.y);
-            if ((sx < 0x1p-62f) & (qs.x != 0.0f)) qc[i].x = fdiv_subnormal_rn(ac[i].x, b.x);
-            if ((sy < 0x1p-62f) & (qs.y != 0.0f)) qc[i].y = fdiv_subnormal_rn(ac[i].y, b.y);
+            const bool subx = (fabsf(qs.x) < 0x1p-62f) & (qs.x != 0.0f);
+            const bool suby = (fabsf(qs.y) < 0x1p-62f) & (qs.y != 0.0f);
+            if (subx | suby) {
+                if (subx) qc[i].x = fdiv_subnormal_rn(ac[i].x, b.x);
+                if (suby) qc[i].y = fdiv_subnormal_rn(ac[i].y, b.y);
+            }
             g = g & (fabsf(ac[i].x) <= 0x1p+36f) & (fabsf(ac[i].y) <= 0x1p+36f);
         }
         ok = ok & g;
