@@ -220,15 +220,23 @@ int g_alt = 1;   // alternate the sweep direction of odd segments (L2 reuse of s
 
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
-    // Rows per CTA segment.  Short segments shrink the tail of the last wave
-    // of CTAs; long ones amortise the 2 halo rows and the pipeline prologue.
-    // Measured on B200 (profiles/r01/seg_sweep.json, fast mode, 1024^2 ..
-    // 16384^2): the best length tracks ny/256, clamped to [8, 32].
-    (void)nbands;
-    (void)ctas_per_sm;
-    int seg = 8;
-    while (seg < 32 && seg * 2 <= ny / 256) seg *= 2;
-    return seg;
+    // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
+    // pipeline prologue; short ones shrink the tail of the last wave.  B200
+    // sweep (profiles/r01/seg_sweep2.json, fast mode, 2048^2 .. 16384^2):
+    // take the longest of 32/24/16/12/8 rows that still gives >= 3 waves of
+    // CTAs; on smaller grids the one whose CTAs fill the last wave best.
+    const int cands[5] = {32, 24, 16, 12, 8};
+    const int64_t slots = 148LL * ctas_per_sm;
+    for (int seg : cands)
+        if ((int64_t)nbands * ((ny + seg - 1) / seg) >= 3 * slots) return seg;
+    int best = 8;
+    double best_fill = -1.0;
+    for (int seg : cands) {
+        const int64_t c = (int64_t)nbands * ((ny + seg - 1) / seg);
+        const double fill = (double)c / (double)(((c + slots - 1) / slots) * slots);
+        if (fill > best_fill + 1e-9) { best_fill = fill; best = seg; }
+    }
+    return best;
 }
 
 template <class T, bool FAST, int RED>
