@@ -298,7 +298,18 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     int fix_rows = 0;
     constexpr int UNR = FAST ? FKC_FAST_UNROLL : FKC_EXACT_UNROLL;  // keep the loop body inside the I-cache
 
-    for (int k = 0; k < nstages; ++k) {
+    // The loop bound is re-derived from %ctaid.y (a volatile read the
+    // compiler cannot hoist) instead of being kept live: in the reduction
+    // variants at the 168-register cap it was otherwise spilled, and with
+    // 3 x 74 KB of shared memory per SM the local-memory reload went to L2
+    // every stage.
+    auto stages_left = [&](int k) {
+        uint32_t cy;
+        asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(cy));
+        const int yy0 = 1 + (int)cy * seg;
+        return k < (min(seg, ny - yy0 + 1) + 2 + R - 1) / R;
+    };
+    for (int k = 0; stages_left(k); ++k) {
         const int s = k % tma::S;
         // refill the slot freed by stage k-1 (every lane finished reading it)
         if (lane == 0 && k + tma::S - 1 < nstages) {
