@@ -437,7 +437,7 @@ class DistributedSimulation:
     """
 
     def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None,
-                 transport: str = "peer"):
+                 transport: str = "peer", state=None):
         import torch
         import torch.distributed as dist
         from . import swdemo
@@ -452,12 +452,16 @@ class DistributedSimulation:
         self.stream = stream
         t = self.tile
         full = Extent(t.nx + 2, t.ny + 2)
-        h = gaussian_tile(grid, rank, cfg.precision, cfg.dx, cfg.dy, cfg.base, cfg.amplitude, cfg.center,
-                          cfg.width)
-        H = Field.zeros(full, cfg.precision)
-        H.data[1:-1, 1:-1] = h
-        st = swdemo.SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
-                            cfg.g, cfg.dx, cfg.dy).to_device(device)
+        if state is None:       # the tile of swdemo.init_state's Gaussian hump
+            h = gaussian_tile(grid, rank, cfg.precision, cfg.dx, cfg.dy, cfg.base, cfg.amplitude, cfg.center,
+                              cfg.width)
+            H = Field.zeros(full, cfg.precision)
+            H.data[1:-1, 1:-1] = h
+            state = swdemo.SWState(H, Field.zeros(full, cfg.precision), Field.zeros(full, cfg.precision),
+                                   cfg.g, cfg.dx, cfg.dy)
+        elif tuple(state.full) != tuple(full):
+            raise ValueError(f"state extent {tuple(state.full)} != tile extent {tuple(full)}")
+        st = state.to_device(device)
         self.a = st
         self.b = swdemo.SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx, st.dy)
         tdt = torch.float32 if cfg.precision == "f32" else torch.float64
@@ -647,21 +651,33 @@ def bench_main(args, rank: int, world: int) -> int:
     # fixed dt = 0.3 * stable_dt of the initial global state (h max 1.4, u = v = 0)
     dt = 0.3 * 1.0 / float(np.sqrt(np.float32(9.8) * np.float32(1.4)))
     cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
+    from bench import ClockSampler
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport)
         sim.advance(args.warmup)
         torch.cuda.synchronize()
         dist.barrier()
+        clocks = ClockSampler(local) if rank == 0 else None
+        if clocks:
+            clocks.__enter__()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         sim.advance(args.steps)
         t1.record(stream)
         torch.cuda.synchronize()
+        if clocks:
+            clocks.__exit__(None, None, None)
         dist.barrier()
     ms = torch.tensor([t0.elapsed_time(t1)], device="cpu" if one_dev else dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
+    launches = sim._launches_per_step()
+    transport, fallback = sim.transport, sim.fallback_reason
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    e2e = None if getattr(args, "no_e2e", False) else _bench_e2e(args, cfg, grid, rank, world, dev, one_dev)
     cells = grid.NX * grid.NY
     value = cells * args.steps / (total_ms / 1e3) / 1e9
     if rank == 0:
@@ -676,17 +692,61 @@ def bench_main(args, rank: int, world: int) -> int:
                 "config": {"workload": workload(n, world),
                            "exchange": "one-cell halo exchange per step " +
                                        ("fused into the step kernel (NVLink peer stores + mailbox flags)"
-                                        if sim.transport == "peer" else "(pack + NCCL send/recv + unpack)"),
+                                        if transport == "peer" else "(pack + NCCL send/recv + unpack)"),
 
                            "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
                 "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
                              "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
-                "gpu_launches": args.steps * sim._launches_per_step()}
-        line["config"]["transport"] = sim.transport
-        if sim.fallback_reason:
-            line["config"]["transport_fallback"] = sim.fallback_reason[:300]
+                "gpu_launches": args.steps * launches,
+                "clocks": clocks.summary()}
+        if e2e is not None:
+            line["e2e"] = e2e
+        line["config"]["transport"] = transport
+        if fallback:
+            line["config"]["transport_fallback"] = fallback[:300]
         print(json.dumps(line))
-    sim.close()
     dist.destroy_process_group()
     return 0
+
+
+def _bench_e2e(args, cfg, grid: CartGrid, rank: int, world: int, dev, one_dev: bool):
+    """End to end through the public API at N GPUs: every rank's tile
+    starts in pinned host memory, DistributedSimulation uploads it, sets up
+    the exchange, advances `steps` steps and the final tile is copied back;
+    wall clock between two barriers, max over ranks."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import swdemo
+    from .field import Field
+    t = grid.tile(rank)
+    full = Extent(t.nx + 2, t.ny + 2)
+    steps = max(args.steps, 200)
+    pin = [torch.zeros((t.ny + 2, t.nx + 2), dtype=torch.float32, pin_memory=True) for _ in range(6)]
+    pin[0][1:-1, 1:-1] = torch.from_numpy(gaussian_tile(grid, rank, "f32", cfg.dx, cfg.dy, cfg.base,
+                                                        cfg.amplitude, cfg.center, cfg.width))
+    host_in = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[:3]), cfg.g, cfg.dx, cfg.dy)
+    host_out = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[3:]), cfg.g, cfg.dx, cfg.dy)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport, state=host_in)
+        sim.advance(steps)
+        sim.state().to_host(host_out)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    sim.close()
+    dist.barrier()
+    tt = torch.tensor([el], dtype=torch.float64, device="cpu" if one_dev else dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    el = float(tt.item())
+    state_bytes = 3 * 4 * (t.nx + 2) * (t.ny + 2) * world
+    return {"value": round(grid.NX * grid.NY * steps / el / 1e9, 3), "unit": "Gcell-updates/s",
+            "h2d_bytes_per_step": round(state_bytes / steps, 1), "d2h_bytes_per_step": round(state_bytes / steps, 1),
+            "steps": steps, "api": "DistributedSimulation(cfg, grid, rank, state=<host pinned tile>) -> "
+                                   "advance(steps) -> state().to_host(<host pinned tile>)"}

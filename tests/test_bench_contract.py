@@ -53,3 +53,4 @@ def test_multi_rank_bench_one_device(nproc, n):
     d = _last_json(r.stdout)
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == nproc and d["config"]["transport"] == "peer" and d["gpu_launches"] == 6
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and "clocks" in d
