@@ -189,6 +189,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", "--grid-n", dest="n", type=int, default=16384, help="cells per side (per GPU)")
+    ap.add_argument("--global-n", type=int, default=0,
+                    help="N>1 strong scaling: a fixed global grid of this many cells per side "
+                         "(BASELINE config 4: 32768) instead of --grid-n per GPU")
     ap.add_argument("--mode", default="fast", choices=["exact", "fast"],
                     help="fast: FMA + approximate reciprocals, as accurate as the f32 oracle (headline); "
                          "exact: bit-identical to the oracle")

@@ -647,7 +647,10 @@ def bench_main(args, rank: int, world: int) -> int:
         dist.init_process_group("nccl", device_id=dev)
     px, py = choose_grid(world)
     n = args.n
-    grid = CartGrid(px, py, px * n, py * n, "reflective")
+    strong = bool(getattr(args, "global_n", 0))
+    # weak scaling (default): n^2 cells per GPU; strong: a fixed global grid
+    grid = CartGrid(px, py, args.global_n, args.global_n, "reflective") if strong else \
+        CartGrid(px, py, px * n, py * n, "reflective")
     # fixed dt = 0.3 * stable_dt of the initial global state (h max 1.4, u = v = 0)
     dt = 0.3 * 1.0 / float(np.sqrt(np.float32(9.8) * np.float32(1.4)))
     cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
@@ -687,9 +690,12 @@ def bench_main(args, rank: int, world: int) -> int:
         from bench import METRIC, workload
         line = {"metric": METRIC, "value": round(value, 3),
                 "unit": "Gcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+                "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
-                "config": {"workload": workload(n, world),
+                "config": {"workload": (f"shallow-water {grid.NX}x{grid.NY} fp32 2-D decomposed {px}x{py}, "
+                                        "reflective, fixed dt=0.3*stable_dt (BASELINE config 4, strong scaling)")
+                           if strong else workload(n, world),
                            "exchange": "one-cell halo exchange per step " +
                                        ("fused into the step kernel (NVLink peer stores + mailbox flags)"
                                         if transport == "peer" else "(pack + NCCL send/recv + unpack)"),
