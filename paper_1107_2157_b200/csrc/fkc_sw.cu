@@ -242,12 +242,14 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
 template <class T, bool FAST, int RED>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
     using G = tma::Geo<T>;
-    static bool attr_set = false;
     auto kern = sw_step_tma<T, FAST, RED>;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
-        attr_set = true;
-    }
+    static std::once_flag attr_once;   // per instantiation; thread-safe
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+    });
+    if (attr_err != cudaSuccess)
+        return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
     const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
     const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
