@@ -310,6 +310,12 @@ int fkc_set_tma_alternate(int on) {
     return FKC_OK;
 }
 
+int fkc_test_div_f64(const double* a, const double* b, double* q, double* qref, int64_t n, void* stream) {
+    if (!a || !b || !q || !qref || n < 0) return fail(FKC_EUSAGE, "bad arguments");
+    test_div64_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, b, q, qref, n);
+    return check_launch("test_div64_kernel");
+}
+
 int fkc_test_div_f32(const float* a, const float* b, float* q, float* qref, int64_t n, void* stream) {
     if (!a || !b || !q || !qref || n < 0) return fail(FKC_EUSAGE, "bad arguments");
     test_div_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, b, q, qref, n);
