@@ -372,8 +372,7 @@ def e2e_run(n, dt, args, dev):
         t = torch.empty((n + 2, n + 2), dtype=torch.float32, pin_memory=True)
         t.copy_(f.data)
         pinned.append(t)
-    del st
-    torch.cuda.empty_cache()
+    del st     # its device blocks stay in torch's caching allocator: run() reuses them (a warm process)
     host_state = swdemo.SWState(*(Field(full, t.numpy(), "f32") for t in pinned))
     out_pinned = [torch.empty((n + 2, n + 2), dtype=torch.float32, pin_memory=True) for _ in range(3)]
     host_out = swdemo.SWState(*(Field(full, t.numpy(), "f32") for t in out_pinned))
@@ -389,6 +388,7 @@ def e2e_run(n, dt, args, dev):
             "steps": steps, "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
             "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel, each step's "
                            "40-byte row copied device->host after the step",
+            "allocator": "warm (device blocks of the setup state cached by torch and reused)",
             "final_mass": res.rows[-1][3]}
 
 
