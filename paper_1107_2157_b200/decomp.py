@@ -429,15 +429,20 @@ def gaussian_tile(grid: CartGrid, rank: int, precision="f32", dx=1.0, dy=1.0, ba
 # ---------------------------------------------------------------------------
 
 class DistributedSimulation:
-    """One rank's tile of a decomposed run: step kernel with per-side BC,
-    then halo exchange of the new state, double-buffer swap.
+    """One rank's tile of a decomposed run: step kernel with per-side BC and
+    the halo exchange (fused peer stores, or NCCL), double-buffer swap.
 
-    ``dt`` is fixed (``cfg.dt``) -- the weak-scaling benchmark; for CFL-driven
-    runs the per-rank bound from the fused reduction is all-reduced (MIN).
+    ``cfg.dt`` fixed: the weak-scaling benchmark.  ``cfg.dt is None``: the
+    SPEC ``run`` across GPUs -- every step's fused
+    reduction writes this tile's CFL bound into a device slot, one 8-byte
+    all-reduce (MIN, stream-ordered: no host synchronisation) makes it the
+    global bound, and the next step reads its dt from that slot on the
+    device.  ``diagnostics=True`` (implied by CFL mode) also keeps the per-step
+    mass / maxima / error words; :meth:`rows` combines them over the ranks.
     """
 
     def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None,
-                 transport: str = "peer", state=None):
+                 transport: str = "peer", state=None, diagnostics: bool = False, capacity=None):
         import torch
         import torch.distributed as dist
         from . import swdemo
@@ -489,30 +494,103 @@ class DistributedSimulation:
             (stream or torch.cuda.current_stream()).synchronize()
             dist.barrier(group)
         self._group = group
+        self.cfl = cfg.dt is None
+        self.diag = diagnostics or self.cfl
+        self.slots = None
+        if self.diag:
+            cap = (capacity if capacity is not None else cfg.steps) + 1
+            self.slots = swdemo.ReductionSlots(cap, st.H.storage.device)
+            red = self.slots.reduce_struct(0)
+            g = swdemo._grid(st.H)
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                N.check(N.lib().fkc_sw_reduce_state(ctypes.byref(g), st.H.ptr, st.U.ptr, st.V.ptr, st.dx, st.dy,
+                                                    st.g, ctypes.byref(red), swdemo._stream_ptr(stream)))
+                if self.cfl:
+                    self._allreduce_bound(0)
+
+    def _allreduce_bound(self, row: int):
+        """Global CFL bound of state `row`: MIN over the ranks of the tiles'
+        bounds (positive doubles stored as int64 bits: integer order = value
+        order), in place in the device slot."""
+        import torch.distributed as dist
+        slot = self.slots.buf[row, 3:4]
+        if dist.get_backend(self._group) == "nccl":
+            dist.all_reduce(slot, op=dist.ReduceOp.MIN, group=self._group)      # stream-ordered on the device
+        else:                                                                    # gloo (tests): via the host
+            h = slot.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MIN, group=self._group)
+            slot.copy_(h)
 
     def _launches_per_step(self) -> int:
         return 1 if self.transport == "peer" else 1 + 2 * len(self.ex.send)
 
     def advance(self, steps: int):
+        import torch
         from . import swdemo
         L = N.lib()
         sp = swdemo._stream_ptr(self.stream)
-        for _ in range(steps):
-            src, dst = (self.a, self.b) if self.n % 2 == 0 else (self.b, self.a)
-            if self.transport == "peer":
-                a = swdemo._step_args(src, dst, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant)
-                out_parity = (self.n + 1) % 2
-                for s, line in self.peer.lines[out_parity].items():
-                    a.peer[s] = line
-                fill_sync(a.sync, self.peer.mail, self.peer.signal, self.n)
-                N.check(L.fkc_sw_step(ctypes.byref(a), sp))
-                dst.t = src.t + float(self.cfg.dt)
-            else:
-                swdemo.advance(src, self.cfg.dt, self.bc, self.cfg.mode, self.cfg.variant, out=dst,
-                               stream=self.stream)
-                self.ex.exchange(dst)
-            self.n += 1
+        cfg = self.cfg
+        if self.diag and self.n + steps >= self.slots.n:
+            raise ValueError("reduction slot capacity exceeded")
+        with torch.cuda.stream(self.stream or torch.cuda.current_stream()):
+            for _ in range(steps):
+                src, dst = (self.a, self.b) if self.n % 2 == 0 else (self.b, self.a)
+                red = self.slots.reduce_struct(self.n + 1, cfl=self.cfl) if self.diag else None
+                bound = self.slots.addr(self.n, 3) if self.cfl else None
+                a = swdemo._step_args(src, dst, cfg.dt if cfg.dt is not None else 0.0, self.bc, cfg.mode,
+                                      cfg.variant, red, bound, cfg.cfl_factor)
+                if self.transport == "peer":
+                    out_parity = (self.n + 1) % 2
+                    for s, line in self.peer.lines[out_parity].items():
+                        a.peer[s] = line
+                    fill_sync(a.sync, self.peer.mail, self.peer.signal, self.n)
+                    N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+                else:
+                    N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+                    self.ex.exchange(dst)
+                if cfg.dt is not None:
+                    dst.t = src.t + float(cfg.dt)
+                self.n += 1
+                if self.cfl:
+                    self._allreduce_bound(self.n)
         return self
+
+    def rows(self):
+        """Global diagnostics rows (step, t, dt, mass, max_hu, max_hv) of the
+        steps so far (collective: sums the tiles' masses, maxima over ranks,
+        error words OR-ed); raises the reference's errors like swdemo.run."""
+        import torch
+        import torch.distributed as dist
+        from . import swdemo
+        if not self.diag:
+            return []
+        (self.stream or torch.cuda.current_stream()).synchronize()
+        d = swdemo.ReductionSlots.decode(self.slots.buf[: self.n + 1].cpu().numpy())
+        mass = torch.tensor(d["mass"], dtype=torch.float64)
+        mx = torch.tensor(np.stack([d["max_hu"], d["max_hv"]]), dtype=torch.float64)
+        e = d["err"].astype(np.int64)
+        err = torch.tensor(np.stack([e & 1, (e >> 1) & 1, (e >> 2) & 1]))   # OR of bits = MAX per bit
+        dev = self.slots.buf.device if dist.get_backend(self._group) == "nccl" else "cpu"
+        mass, mx, err = mass.to(dev), mx.to(dev), err.to(dev)
+        dist.all_reduce(mass, op=dist.ReduceOp.SUM, group=self._group)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self._group)
+        dist.all_reduce(err, op=dist.ReduceOp.MAX, group=self._group)
+        mass, mx = mass.cpu().numpy(), mx.cpu().numpy()
+        eb = err.cpu().numpy()
+        err = eb[0] | (eb[1] << 1) | (eb[2] << 2)
+        cfg = self.cfg
+        f = np.float32 if cfg.precision == "f32" else np.float64
+        out, t = [], 0.0
+        if err[0]:
+            swdemo.raise_for_error(int(err[0]), "in the initial state")
+        for k in range(self.n):
+            if err[k + 1]:
+                swdemo.raise_for_error(int(err[k + 1]), f"at step {k + 1}")
+            dt = float(cfg.dt) if cfg.dt is not None else float(f(cfg.cfl_factor) * f(d["cfl_min"][k]))
+            t += dt
+            out.append((k + 1, t, dt, float(mass[k + 1]) * cfg.dx * cfg.dy, float(mx[0, k + 1]),
+                        float(mx[1, k + 1])))
+        return out
 
     def close(self):
         """Drain, then unmap the neighbours' memory (collective)."""
