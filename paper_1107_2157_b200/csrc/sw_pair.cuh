@@ -239,6 +239,23 @@ __device__ __forceinline__ float2 pmul2(float2 a, float2 b) { return __fmul2_rn(
 // DIV_GUARD clears ok when an operand is outside that (b outside
 // [2^-24, 2^24], |a| too large, inf / nan);
 // DIV_FIXUP is the scalar never-failing path for such rows.
+// RN(a / b) for a subnormal quotient, from the correctly rounded SCALED
+// quotient qs = RN24(a 2^64 / b) (|qs| < 2^-62, qs != 0, b > 0 in range):
+// T = |qs| 2^85 is exactly RN24(t) with t = |a| 2^149 / b < 2^23, so the
+// closed form of sw_math.cuh fdiv_subnormal_rn applies without redoing the
+// division -- RN_int(T) unless T is a half-integer, where the sign of the
+// exact residual fma(-b, T, |a| 2^149) decides.
+__device__ __forceinline__ float subnormal_from_scaled(float a, float b, float qs) {
+    const float T = fabsf(qs) * 0x1p85f;
+    const float fl = floorf(T);
+    float k = rintf(T);
+    if (T - fl == 0.5f) {
+        const float e = __fmaf_rn(-b, T, (fabsf(a) * 0x1p100f) * 0x1p49f);
+        k = e > 0.0f ? fl + 1.0f : (e < 0.0f ? fl : k);
+    }
+    return __uint_as_float((__float_as_uint(a) & 0x80000000u) | (uint32_t)k);
+}
+
 template <int DM, int NF, int NC>
 __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const float2 (&ac)[NC], float2 (&qf)[NF],
                                      float2 (&qc)[NC], bool absorb, bool& ok) {
@@ -269,8 +286,8 @@ __device__ __forceinline__ void div2(float2 b, const float2 (&af)[NF], const flo
             const bool subx = (fabsf(qs.x) < 0x1p-62f) & (qs.x != 0.0f);
             const bool suby = (fabsf(qs.y) < 0x1p-62f) & (qs.y != 0.0f);
             if (subx | suby) {
-                if (subx) qc[i].x = fdiv_subnormal_rn(ac[i].x, b.x);
-                if (suby) qc[i].y = fdiv_subnormal_rn(ac[i].y, b.y);
+                if (subx) qc[i].x = subnormal_from_scaled(ac[i].x, b.x, qs.x);
+                if (suby) qc[i].y = subnormal_from_scaled(ac[i].y, b.y, qs.y);
             }
             g = g & (fabsf(ac[i].x) <= 0x1p+36f) & (fabsf(ac[i].y) <= 0x1p+36f);
         }
