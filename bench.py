@@ -161,7 +161,7 @@ def numpy_sample(n, rows):
 # ---------------------------------------------------------------------------
 
 def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, boundary="reflective",
-                          precision="f32"):
+                          precision="f32", amplitude=0.4):
     """Gaussian-hump initial state built on the device (setup only)."""
     import torch
     from paper_1107_2157_b200 import swdemo
@@ -175,7 +175,7 @@ def device_gaussian_state(n_x, n_y, device, x_off=0, y_off=0, n_glob=None, bound
     w = ng_x / 8.0
     for r0 in range(0, n_y, 2048):          # chunk to bound f64 temporaries
         r1 = min(n_y, r0 + 2048)
-        h = 1.0 + 0.4 * torch.exp(-(xs[None, :] ** 2 + ys[r0:r1, None] ** 2) / (w * w))
+        h = 1.0 + amplitude * torch.exp(-(xs[None, :] ** 2 + ys[r0:r1, None] ** 2) / (w * w))
         H.data[1 + r0:1 + r1, 1:-1] = h.to(torch.float32 if precision == "f32" else torch.float64)
     st = swdemo.SWState(H, U, V)
     swdemo.apply_boundary(st, boundary)
@@ -209,6 +209,8 @@ def main():
                     help="fused reductions in the timed steps: none; diag = mass, max|hu|, max|hv|, error word "
                          "(run()'s per-step diagnostics); cfl = diag + the CFL bound, dt recomputed on device "
                          "every step (SPEC.md:529-537 run)")
+    ap.add_argument("--amplitude", type=float, default=0.4,
+                    help="Gaussian hump amplitude of the synthetic state (0: a lake at rest; profiling only)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the other-mode timing (profiling runs)")
@@ -253,7 +255,7 @@ def main():
     if args.seg:
         N.check(N.lib().fkc_set_tma_segment(args.seg))
     N.check(N.lib().fkc_set_tma_alternate(args.alt))
-    st = device_gaussian_state(n, n, dev, precision=args.precision)
+    st = device_gaussian_state(n, n, dev, precision=args.precision, amplitude=args.amplitude)
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0
     r = time_steps(st, n, dt, args.mode, args.variant, args.steps, args.warmup, sample_clocks=True,
