@@ -37,7 +37,7 @@ constexpr int WARPS = 4;                 // warps (strips) per CTA
 #define FKC_TMA_CTAS_FAST_RED 3  // fast kernel with fused reductions
 #endif
 #ifndef FKC_TMA_CTAS_EXACT
-#define FKC_TMA_CTAS_EXACT 2  // exact kernel: ~190 registers -> 8 warps per SM
+#define FKC_TMA_CTAS_EXACT 3  // exact kernel: <= 168 registers -> 12 warps per SM (no spills)
 #endif
 constexpr int R = FKC_TMA_R;             // rows per stage
 constexpr int S = FKC_TMA_S;             // ring stages per warp
