@@ -36,6 +36,9 @@ constexpr int WARPS = 4;                 // warps (strips) per CTA
 #ifndef FKC_TMA_CTAS_FAST_RED
 #define FKC_TMA_CTAS_FAST_RED 3  // fast kernel with fused reductions
 #endif
+#ifndef FKC_TMA_CTAS_F64
+#define FKC_TMA_CTAS_F64 2    // f64 kernels (~190-210 registers)
+#endif
 #ifndef FKC_TMA_CTAS_EXACT
 #define FKC_TMA_CTAS_EXACT 3  // exact kernel: <= 168 registers -> 12 warps per SM (no spills)
 #endif
@@ -52,7 +55,7 @@ template <class T> struct Geo {
     static constexpr int WARP_RING = S * STAGE_BYTES;
     static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
     template <bool FAST, int RED = 0> static constexpr int ctas_per_sm() {
-        return sizeof(T) == 8 ? 2 : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT);
+        return sizeof(T) == 8 ? FKC_TMA_CTAS_F64 : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT);
     }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
