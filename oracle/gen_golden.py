@@ -18,7 +18,10 @@ Fixtures (npz, full (ny+2, nx+2) arrays incl. halos):
 * ``hand4_periodic_f64.npz`` -- SPEC.md:528's "4x4 periodic hand oracle":
   a pure-Python scalar evaluation of SPEC.md:521-522 on a 4x4 grid.
 
-Usage:  python oracle/gen_golden.py   (writes tests/golden/*.npz)
+* ``spec64_f64_{reflective,periodic}.npz`` -- SPEC.md's f64 acceptance
+  setting: 64x64 f64, CFL 0.9 recomputed every step, 100 steps.
+
+Usage:  python oracle/gen_golden.py [spec64]   (writes tests/golden/*.npz)
 """
 
 from __future__ import annotations
@@ -138,5 +141,36 @@ def main():
                         1.0 / math.sqrt(9.8), rel_tol=0, abs_tol=1e-15)
 
 
+def spec64():
+    """``spec64_f64_<bc>.npz`` -- SPEC.md's f64 acceptance setting
+    (SPEC.md:648-651): 64x64 f64 Gaussian hump, CFL 0.9 recomputed every
+    step, 100 steps, per boundary mode: inputs, states after 1 and 100
+    steps, the dt series and the diagnostics rows (AST evaluator over the
+    reference parser/sema, cross-checked against the numpy oracle)."""
+    cp = dsl_eval.load_checked(FK)
+    n = 64
+    for bc in ("reflective", "periodic"):
+        H, U, V = so.init_state(n, n, "f64", boundary=bc)
+        st, dts, rows, t, step1 = (H, U, V), [], [], 0.0, None
+        for k in range(100):
+            dt = so.stable_dt(*st, 1.0, 1.0, cfl=0.9)
+            st = dsl_step(cp, *st, 1.0, 1.0, dt, bc)
+            t += dt
+            dts.append(dt)
+            rows.append((k + 1, t, dt) + so.diagnostics(*st))
+            if k == 0:
+                step1 = tuple(a.copy() for a in st)
+        ref = so.run(H, U, V, 100, cfl=0.9, boundary=bc)
+        assert all(np.array_equal(a, b) for a, b in zip(st, (ref.H, ref.U, ref.V)))
+        np.savez_compressed(os.path.join(OUT, f"spec64_f64_{bc}.npz"),
+                            H0=H, U0=U, V0=V, H1=step1[0], U1=step1[1], V1=step1[2],
+                            H100=st[0], U100=st[1], V100=st[2], dt=np.array(dts), rows=np.array(rows))
+        print("spec64", bc, "final mass", rows[-1][3], "mass drift", rows[-1][3] / rows[0][3] - 1)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "spec64":
+        spec64()
+    else:
+        main()
+        spec64()

@@ -163,3 +163,17 @@ def test_numpy_oracle_equals_ast_evaluator(prec):
     ref = so.wave_advance(0.8, 1.1, 0.07, H, U, V)
     for k, b in zip(("oh", "ou", "ov"), ref):
         assert np.array_equal(outs[k][1:-1, 1:-1], b)
+
+
+@pytest.mark.parametrize("bc", ["reflective", "periodic"])
+def test_golden_spec64_f64(bc):
+    """SPEC.md's f64 acceptance setting (64x64, CFL 0.9, 100 steps): the
+    oracle's run reproduces the fixture made with the reference parser/sema,
+    and mass is conserved to 1e-12."""
+    from conftest import load_golden
+    g = load_golden(f"spec64_f64_{bc}.npz")
+    r = so.run(g["H0"], g["U0"], g["V0"], 100, cfl=0.9, boundary=bc)
+    assert np.array_equal(r.H, g["H100"]) and np.array_equal(r.U, g["U100"]) and np.array_equal(r.V, g["V100"])
+    assert np.array_equal(np.array([row[2] for row in r.rows]), g["dt"])
+    m = g["rows"][:, 3]
+    assert abs(m[-1] - so.total_mass(g["H0"])) / m[-1] <= 1e-12
