@@ -446,7 +446,7 @@ class DistributedSimulation:
         import torch
         import torch.distributed as dist
         from . import swdemo
-        from .field import DeviceField, Field
+        from .field import Field
         if transport not in ("peer", "nccl", "auto"):
             raise ValueError(f"unknown transport {transport!r}")
         self.fallback_reason = None

@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _native as N
-from .field import DeviceField, dtype_of
+from .field import DeviceField
 from .region import Extent, Halo, HaloTooLarge, interior_of
 
 

@@ -21,7 +21,6 @@ kernel and the reduction kernel.
 from __future__ import annotations
 
 import ctypes
-import math
 from dataclasses import dataclass, field as dc_field
 from typing import List, Optional, Sequence, Tuple, Union
 
@@ -29,7 +28,7 @@ import numpy as np
 
 from . import _native as N
 from .field import DeviceField, Field, dtype_of
-from .region import Extent, Halo
+from .region import Extent
 
 BC_CODES = {"reflective": N.BC_REFLECTIVE, "periodic": N.BC_PERIODIC, "none": N.BC_NONE}
 MODES = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}
