@@ -121,3 +121,28 @@ def test_sm100a_sass_present():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_integration_c_example_compiles_and_links():
+    """The C snippet of INTEGRATION.md section 3 compiles against
+    include/fkc_sw.h and links against the library; run without a GPU it
+    reports the usage error for null pointers (no device touched)."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = doc[doc.index("## 3. C / C++ callers"):]
+    snippet = sec[sec.index("```c") + 4:sec.index("```", sec.index("```c") + 4)]
+    main = r"""
+    int main(void) {
+        int rc = one_step(8, 8, 32, 0, 0, 0, 0, 0, 0, 0.1, 0);
+        return rc == FKC_EUSAGE ? 0 : 1;
+    }
+    """
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "ex.c")
+        open(c, "w").write(snippet + main)
+        exe = os.path.join(d, "ex")
+        libdir = os.path.dirname(N.LIB_PATH)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe, "-L", libdir, "-lfkc_sw",
+                        f"-Wl,-rpath,{libdir}"], check=True)
+        r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "null" in r.stderr
