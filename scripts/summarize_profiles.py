@@ -103,6 +103,10 @@ def launch_shares(src, dst):
     T = sum(tot.values())
     out = ["# Launch list of `python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-other`",
            "", "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised).", "",
+           "The timed region of bench.py launches only `sw_step_tma` (one launch per step: 5 warm-up + 20 timed "
+           "here); every other kernel below is setup outside it (the Gaussian initial state built with torch "
+           "elementwise ops, the initial halo fill, the stable_dt reduction that fixes dt).  Share of the "
+           "step kernel in the TIMED region: 100 %.", "",
            "| kernel | launches | total ms | share | avg us |", "|---|---|---|---|---|"]
     for k, v in tot.most_common():
         out.append(f"| `{k[:70]}` | {cnt[k]} | {v / 1e6:.3f} | {v / T * 100:.1f}% | {v / cnt[k] / 1e3:.1f} |")
