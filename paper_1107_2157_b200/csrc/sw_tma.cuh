@@ -1,5 +1,6 @@
 // sw_tma.cuh -- the product kernel: per-warp TMA y-sweep of the fused
-// two-step Lax-Wendroff step (f32).
+// two-step Lax-Wendroff step (f32 and f64; fast and bit-exact modes; fused
+// boundary halos, reductions and multi-GPU halo exchange).
 //
 // Geometry.  A warp owns a strip of OWN = 30*CPL columns and `seg` rows.
 // It loads LOAD = 32*CPL columns (the strip plus CPL columns on each side):
@@ -18,6 +19,11 @@
 // left of its first cell is lane-1's last face (shfl.up).  The row above is
 // then updated and stored with vector stores; the output halo (boundary
 // conditions) and optional reductions are emitted in the same pass.
+//
+// The per-row arithmetic lives in the row engines of sw_pair.cuh
+// (PairEngine: f32 fast on the packed FP32 pipe; ExactPairEngine: f32
+// bit-exact; ScalarEngine: f64).  In fast mode odd segments sweep the mirror
+// image top-down (L2 reuse of the rows shared by neighbouring segments).
 #pragma once
 #include "sw_pair.cuh"
 
