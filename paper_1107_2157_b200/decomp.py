@@ -608,7 +608,7 @@ class DistributedSimulation:
 
 
 def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchange: str = "pack",
-                         concurrent: bool = False):
+                         concurrent: bool = False, warmup: int = 0, timing: Optional[list] = None):
     """All px*py tiles in one process on one device: the GPU-side validation
     of the decomposed path.  Returns (grid, the tiles' states).
 
@@ -643,11 +643,20 @@ def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchang
                for r in range(grid.size)]
         lt = LocalTransport(grid)
         lt.exchange_all(exs, states)
-        for _ in range(steps):
+        ev = None
+        for k in range(warmup + steps):
+            if k == warmup and timing is not None:
+                torch.cuda.synchronize()
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                ev[0].record()
             for r in range(grid.size):
                 swdemo.advance(states[r], cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant, out=others[r])
             states, others = others, states
             lt.exchange_all(exs, states)
+        if ev is not None:
+            ev[1].record()
+            torch.cuda.synchronize()
+            timing.append(ev[0].elapsed_time(ev[1]))
         return grid, states
 
     dev = bufs[0][0].H.storage.device
@@ -671,7 +680,15 @@ def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchang
     mails = [Mailbox(dev) for _ in range(grid.size)] if concurrent else None
     streams = [torch.cuda.Stream(dev) for _ in range(grid.size)] if concurrent else None
     L = N.lib()
-    for k in range(steps):
+    ev = None
+    for k in range(warmup + steps):
+        if k == warmup and timing is not None:     # time the last `steps` steps: all tiles, all streams
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(1 + grid.size)]
+            ev[0].record()
+            if concurrent:
+                for st in streams:
+                    st.wait_event(ev[0])
         for r in range(grid.size):
             src, dst = bufs[r][k % 2], bufs[r][(k + 1) % 2]
             a = swdemo._step_args(src, dst, cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant)
@@ -684,8 +701,14 @@ def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchang
             else:
                 sp = torch.cuda.current_stream(dev).cuda_stream
             N.check(L.fkc_sw_step(ctypes.byref(a), sp))
+    if ev is not None:
+        cur = torch.cuda.current_stream(dev)
+        for r in range(grid.size):
+            ev[1 + r].record(streams[r] if concurrent else cur)
+        torch.cuda.synchronize()
+        timing.append(max(ev[0].elapsed_time(e) for e in ev[1:]))
     torch.cuda.synchronize()
-    return grid, [b[steps % 2] for b in bufs]
+    return grid, [b[(warmup + steps) % 2] for b in bufs]
 
 
 def gather_interior(grid: CartGrid, tiles: Sequence[np.ndarray]) -> np.ndarray:
