@@ -239,6 +239,25 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     return best;
 }
 
+int g_tail_seg = -1;    // tail segment rows (-1 auto, 0 off)
+int g_tail_waves = 1;   // CTA waves of tail segments
+
+// Guided segmentation: the last ~g_tail_waves waves of CTAs get short
+// segments of `tail` rows.
+SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0};
+    int tail = g_tail_seg < 0 ? m.seg / 2 : g_tail_seg;
+    if (tail <= 0 || tail >= m.seg || g_seg_override > 0) return m;
+    const int64_t slots = 148LL * ctas_per_sm;
+    // tail rows: enough segments to fill g_tail_waves waves of CTAs
+    const int64_t tail_segs = (g_tail_waves * slots + nbands - 1) / nbands;
+    const int64_t tail_rows = tail_segs * tail;
+    if (tail_rows >= ny / 2) return m;   // small grid: keep it uniform
+    m.jt = (int)((ny - tail_rows) / m.seg);
+    m.tail = tail;
+    return m;
+}
+
 template <class T, bool FAST, int RED>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
     using G = tma::Geo<T>;
@@ -253,10 +272,11 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const fkc_grid& g = a->grid;
     const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
     const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
-    const int seg = pick_seg(nbands, g.ny, G::template ctas_per_sm<FAST>());
-    dim3 grd(nbands, (g.ny + seg - 1) / seg);
+    const SegMap sm = pick_segmap(nbands, g.ny, G::template ctas_per_sm<FAST>());
+    const int nseg = sm.tail == 0 ? (g.ny + sm.seg - 1) / sm.seg : sm.jt + (g.ny - sm.jt * sm.seg + sm.tail - 1) / sm.tail;
+    dim3 grd(nbands, nseg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, seg, g_alt, (T*)a->oH,
+    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, sm, g_alt, (T*)a->oH,
                                                    (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
                                                    to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
@@ -300,6 +320,15 @@ int fkc_abi_version(void) { return FKC_ABI_VERSION; }
 int fkc_set_tma_segment(int seg) {
     if (seg < 0) return fail(FKC_EUSAGE, "segment must be >= 0");
     g_seg_override = seg;
+    return FKC_OK;
+}
+
+// test hook: guided segmentation -- tail segment rows (-1 auto = half the
+// segment, 0 off) and how many CTA waves of them
+int fkc_set_tma_tail(int rows, int waves) {
+    if (rows < -1 || waves < 1 || waves > 64) return fail(FKC_EUSAGE, "tail rows must be >= -1 and waves in 1..64");
+    g_tail_seg = rows;
+    g_tail_waves = waves;
     return FKC_OK;
 }
 

@@ -160,6 +160,19 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
     tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
 }
 
+// Row segments of the CTA grid's y dimension: segments 0 .. jt-1 are `seg`
+// rows, the rest `tail` rows (tail = 0: all `seg`).  Short tail segments are
+// launched last, so the CTAs of the final, partial wave are short and the
+// idle tail of the step shrinks ("guided" segmentation).
+struct SegMap {
+    int seg, tail, jt;
+};
+__device__ __forceinline__ void seg_rows(const SegMap& m, int j, int ny, int& y0, int& nrows) {
+    const int r0 = (m.tail == 0 || j < m.jt) ? j * m.seg : m.jt * m.seg + (j - m.jt) * m.tail;
+    y0 = 1 + r0;
+    nrows = min((m.tail == 0 || j < m.jt) ? m.seg : m.tail, ny - r0);
+}
+
 template <class T, int CPL> struct Row3 {
     T h[CPL], u[CPL], v[CPL];
 };
@@ -216,7 +229,7 @@ __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int
 template <class T, bool FAST, int RED>
 __global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST, RED>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
-            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, int seg, int alt,
+            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, SegMap sm, int alt,
             T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
             T dx, T dy, DtSrc dts, T g, const __grid_constant__ BCs bc, RedPtrs red,
             const __grid_constant__ Peers P, SyncArgs sy) {
@@ -235,8 +248,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
     const int tx = xs + CPL - 1;                         // its tensor column
     if (xs + CPL > nx) return;                           // strip owns nothing (ragged last band)
-    const int y0 = 1 + blockIdx.y * seg;                 // first interior row of the segment
-    const int nrows = min(seg, ny - y0 + 1);
+    int y0, nrows;                                       // first interior row of the segment, rows
+    seg_rows(sm, blockIdx.y, ny, y0, nrows);
     const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
     const int nstages = (nload + R - 1) / R;
     // Sweep direction (fast mode): with `alt`, odd segments sweep top-down,
@@ -318,8 +331,9 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     auto stages_left = [&](int k) {
         uint32_t cy;
         asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(cy));
-        const int yy0 = 1 + (int)cy * seg;
-        return k < (min(seg, ny - yy0 + 1) + 2 + R - 1) / R;
+        int yy0, nr;
+        seg_rows(sm, (int)cy, ny, yy0, nr);
+        return k < (nr + 2 + R - 1) / R;
     };
     for (int k = 0; stages_left(k); ++k) {
         const int s = k % tma::S;
