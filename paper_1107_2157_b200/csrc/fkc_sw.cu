@@ -193,6 +193,28 @@ bool tma_eligible(const fkc_sw_step_args* a) {
     return peers_tma_ok(a, es);
 }
 
+int g_pdl = 1;   // launch the step kernels with programmatic stream serialisation
+
+// Launch with programmatic dependent launch (see pdl_wait in sw_kernels.cuh).
+// `pdl` false: plain launch -- for grids below ~512^2 (B200, CUDA graphs: the
+// programmatic edge costs more than it hides, 256^2 fast 26 -> 20 Gcell/s)
+// and with the fused exchange (CTAs parked in griddepcontrol.wait must not
+// hold SMs a neighbour tile's kernel on the same GPU needs).
+template <class... KArgs, class... Args>
+void launch_step(void (*kern)(KArgs...), dim3 grd, dim3 blk, size_t smem, cudaStream_t st, bool pdl, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grd;
+    cfg.blockDim = blk;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (g_pdl && pdl) ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <class T>
 int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     const fkc_grid& g = a->grid;
@@ -202,14 +224,15 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     dim3 grd((g.nx + 63) / 64, (g.ny + 3) / 4);
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(red);
+    const bool pdl = (int64_t)g.nx * g.ny >= (1 << 18) && a->sync.counter == nullptr;
 #define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
                  (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red, to_peers(a), to_sync(a)
     if (fast) {
-        if (r) sw_step_generic<T, DIV_FAST, true><<<grd, blk, 0, st>>>(GEN_ARGS);
-        else sw_step_generic<T, DIV_FAST, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+        if (r) launch_step(sw_step_generic<T, DIV_FAST, true>, grd, blk, 0, st, pdl, GEN_ARGS);
+        else launch_step(sw_step_generic<T, DIV_FAST, false>, grd, blk, 0, st, pdl, GEN_ARGS);
     } else {
-        if (r) sw_step_generic<T, DIV_IEEE, true><<<grd, blk, 0, st>>>(GEN_ARGS);
-        else sw_step_generic<T, DIV_IEEE, false><<<grd, blk, 0, st>>>(GEN_ARGS);
+        if (r) launch_step(sw_step_generic<T, DIV_IEEE, true>, grd, blk, 0, st, pdl, GEN_ARGS);
+        else launch_step(sw_step_generic<T, DIV_IEEE, false>, grd, blk, 0, st, pdl, GEN_ARGS);
     }
 #undef GEN_ARGS
     return check_launch("sw_step_generic");
@@ -276,9 +299,9 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const int nseg = sm.tail == 0 ? (g.ny + sm.seg - 1) / sm.seg : sm.jt + (g.ny - sm.jt * sm.seg + sm.tail - 1) / sm.tail;
     dim3 grd(nbands, nseg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    kern<<<grd, tma::THREADS, G::SMEM_BYTES, st>>>(m[0], m[1], m[2], g.nx, g.ny, g.pitch, sm, g_alt, (T*)a->oH,
-                                                   (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
-                                                   to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));
+    launch_step(kern, grd, dim3(tma::THREADS), G::SMEM_BYTES, st, a->sync.counter == nullptr, m[0], m[1], m[2], g.nx, g.ny, g.pitch, sm, g_alt,
+                (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g, to_bcs(a->bc), to_red(a->red),
+                to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
 }
 
@@ -329,6 +352,13 @@ int fkc_set_tma_tail(int rows, int waves) {
     if (rows < -1 || waves < 1 || waves > 64) return fail(FKC_EUSAGE, "tail rows must be >= -1 and waves in 1..64");
     g_tail_seg = rows;
     g_tail_waves = waves;
+    return FKC_OK;
+}
+
+// test hook: programmatic dependent launch of the step kernels (1, default) or plain launches (0)
+int fkc_set_pdl(int on) {
+    if (on != 0 && on != 1) return fail(FKC_EUSAGE, "pdl must be 0 or 1");
+    g_pdl = on;
     return FKC_OK;
 }
 

@@ -278,10 +278,14 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         if (strip == 0) sides |= 1u << SIDE_L;
         if (G::OWN * (strip + 1) >= nx) sides |= 1u << SIDE_R;
     }
+    pdl_launch_dependents();
     if (lane == 0) {
-        if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
         for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait();                                   // the previous step's output is complete
+    if (lane == 0) {
+        if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
         for (int k = 0; k < tma::S - 1 && k < nstages; ++k)
             issue_stage<T>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, stage_y(k));
     }
