@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): every kernel of the library on small grids -- TMA step (exact,
-fast, with reductions, f32 / f64, both sweep directions), generic step,
+fast, with reductions, f32 / f64, both sweep directions, guided tail
+segments, chained launches), generic step,
 boundary fill, reductions, region ops, halo pack / unpack, and the fused
 exchange on four local tiles with concurrent streams."""
 
@@ -44,6 +45,15 @@ def main():
         refinterp.cshift(st.U, 1, 3)
     N.check(N.lib().fkc_set_tma_segment(0))
     N.check(N.lib().fkc_set_tma_alternate(1))
+    # guided segmentation (short tail segments) on a tall grid, chained steps
+    # (programmatic dependent launch between them)
+    H, U, V = so.random_state(128, 4000, "f32", seed=4)
+    st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, "f32")) for a in (H, U, V)))
+    N.check(N.lib().fkc_set_tma_tail(2, 1))
+    for mode in ("exact", "fast"):
+        out = swdemo.advance(st, 0.05, "reflective", mode, "tma")
+        swdemo.advance(out, 0.05, "reflective", mode, "tma")
+    N.check(N.lib().fkc_set_tma_tail(-1, 1))
     for ex, conc in (("pack", False), ("fused", False), ("fused", True)):
         cfg = swdemo.SWConfig(nx=480, ny=256, dt=0.05, boundary="periodic", mode="fast")
         run_local_decomposed(cfg, 2, 2, 3, exchange=ex, concurrent=conc)
