@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 #include <string>
 
@@ -262,13 +263,29 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     return best;
 }
 
+int g_rev_mode = 2;     // segment order: 0 bottom-up, 1 top-down, 2 alternate per launch on a stream
+std::mutex g_rev_mu;
+std::unordered_map<cudaStream_t, int> g_rev;
+
+// Alternate the segment order per launch on a stream, so each step starts
+// with the rows its predecessor wrote last (still in L2).  Evaluated on the
+// host at launch (or capture) time; a captured graph of an even number of
+// steps keeps alternating across replays.
+int next_rev(cudaStream_t st) {
+    if (g_rev_mode != 2) return g_rev_mode;
+    std::lock_guard<std::mutex> lk(g_rev_mu);
+    int& r = g_rev[st];
+    r ^= 1;
+    return r;
+}
+
 int g_tail_seg = -1;    // tail segment rows (-1 auto, 0 off)
 int g_tail_waves = 1;   // CTA waves of tail segments
 
 // Guided segmentation: the last ~g_tail_waves waves of CTAs get short
 // segments of `tail` rows.
 SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
-    SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0};
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0, 0};
     int tail = g_tail_seg < 0 ? m.seg / 2 : g_tail_seg;
     if (tail <= 0 || tail >= m.seg || g_seg_override > 0) return m;
     const int64_t slots = 148LL * ctas_per_sm;
@@ -295,7 +312,8 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     const fkc_grid& g = a->grid;
     const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
     const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
-    const SegMap sm = pick_segmap(nbands, g.ny, G::template ctas_per_sm<FAST>());
+    SegMap sm = pick_segmap(nbands, g.ny, G::template ctas_per_sm<FAST>());
+    sm.rev = next_rev(st);
     const int nseg = sm.tail == 0 ? (g.ny + sm.seg - 1) / sm.seg : sm.jt + (g.ny - sm.jt * sm.seg + sm.tail - 1) / sm.tail;
     dim3 grd(nbands, nseg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
@@ -359,6 +377,14 @@ int fkc_set_tma_tail(int rows, int waves) {
 int fkc_set_pdl(int on) {
     if (on != 0 && on != 1) return fail(FKC_EUSAGE, "pdl must be 0 or 1");
     g_pdl = on;
+    return FKC_OK;
+}
+
+// test hook: order of the TMA kernel's row segments -- 0 bottom-up, 1
+// top-down, 2 alternating per launch on a stream (default)
+int fkc_set_tma_order(int mode) {
+    if (mode < 0 || mode > 2) return fail(FKC_EUSAGE, "order must be 0, 1 or 2");
+    g_rev_mode = mode;
     return FKC_OK;
 }
 

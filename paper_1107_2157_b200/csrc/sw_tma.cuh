@@ -122,11 +122,36 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity, uint32_t*
         if ((spins & 255u) == 0 && clock64() - t0 > 4000000000ll) watchdog_fire(err);
     }
 }
+#ifndef FKC_L2_HINTS
+#define FKC_L2_HINTS 0
+#endif
+// L2 eviction hints (FKC_L2_HINTS, off): inputs streamed in evict-first,
+// the new state stored evict-last, so that the rows of step n's output left
+// in L2 at its end are not displaced by step n's input lines and step n+1
+// (which starts with them, see SegMap::rev) hits them.  Measured on B200:
+// no gain at 2048^2 .. 4096^2 and 8-10 % slower from 5792^2 up (fast mode).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+#if FKC_L2_HINTS
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        :: "r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar), "l"(l2_policy_evict_first()) : "memory");
+#else
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];"
         :: "r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar) : "memory");
+#endif
 }
 
 // One lane's 16-byte vector of a row (4 floats or 2 doubles): shared-memory
@@ -148,6 +173,20 @@ __device__ __forceinline__ void stg_vec(T* p, const T (&v)[CPL], T sgn = T(1)) {
     else
         *(double2*)p = make_double2(sgn * v[0], sgn * v[1]);
 }
+// the new state's row store (evict-last with FKC_L2_HINTS)
+template <class T, int CPL>
+__device__ __forceinline__ void stg_row(T* p, const T (&v)[CPL]) {
+#if FKC_L2_HINTS
+    if constexpr (sizeof(T) == 4)
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                     :: "l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(l2_policy_evict_last()) : "memory");
+    else
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+                     :: "l"(p), "d"(v[0]), "d"(v[1]), "l"(l2_policy_evict_last()) : "memory");
+#else
+    stg_vec<T, CPL>(p, v);
+#endif
+}
 
 // One stage = R rows x LOAD columns of H, U, V (3 boxes), completing on `bar`.
 template <class T>
@@ -163,14 +202,18 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
 // Row segments of the CTA grid's y dimension: segments 0 .. jt-1 are `seg`
 // rows, the rest `tail` rows (tail = 0: all `seg`).  Short tail segments are
 // launched last, so the CTAs of the final, partial wave are short and the
-// idle tail of the step shrinks ("guided" segmentation).
+// idle tail of the step shrinks ("guided" segmentation).  With `rev` the
+// segments are laid out from the top row down (the mirror image), so a step
+// starts where the previous one ended: its first CTAs read rows the previous
+// step wrote last, which are still in L2 (the host alternates `rev` per
+// launch on a stream).
 struct SegMap {
-    int seg, tail, jt;
+    int seg, tail, jt, rev;
 };
 __device__ __forceinline__ void seg_rows(const SegMap& m, int j, int ny, int& y0, int& nrows) {
     const int r0 = (m.tail == 0 || j < m.jt) ? j * m.seg : m.jt * m.seg + (j - m.jt) * m.tail;
-    y0 = 1 + r0;
     nrows = min((m.tail == 0 || j < m.jt) ? m.seg : m.tail, ny - r0);
+    y0 = m.rev ? ny + 1 - r0 - nrows : 1 + r0;     // rows y0 .. y0 + nrows - 1
 }
 
 template <class T, int CPL> struct Row3 {
@@ -406,9 +449,9 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 }
                 const int64_t off = row_off;
                 if (owner && upd) {
-                    stg_vec<T, CPL>(oH + off, oh);
-                    stg_vec<T, CPL>(oU + off, ou);
-                    stg_vec<T, CPL>(oV + off, ov);
+                    stg_row<T, CPL>(oH + off, oh);
+                    stg_row<T, CPL>(oU + off, ou);
+                    stg_row<T, CPL>(oV + off, ov);
                     // output halo (boundary conditions) and fused halo exchange:
                     // tile-edge lanes only, out of line to keep the sweep loop small
                     if ((edge_rows && (y == 1 || y == ny)) || edge_cols) {
