@@ -24,6 +24,13 @@
 // (PairEngine: f32 fast on the packed FP32 pipe; ExactPairEngine: f32
 // bit-exact; ScalarEngine: f64).  In fast mode odd segments sweep the mirror
 // image top-down (L2 reuse of the rows shared by neighbouring segments).
+//
+// Schedule (host side, fkc_sw.cu): a 2-D grid of CTAs = bands of 4 strips x
+// row segments; the last wave's segments are half length (SegMap::tail),
+// successive launches on a stream lay the segments out bottom-up and
+// top-down in turn (SegMap::rev: a step starts on the rows its predecessor
+// wrote last), and launches are programmatic (pdl_wait before the first read
+// of the previous step's output).
 #pragma once
 #include "sw_pair.cuh"
 
