@@ -330,7 +330,7 @@ int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
     const void* ps[3] = {a->H, a->U, a->V};
     int rc;
     for (int f = 0; f < 3; ++f)
-        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<T>::LOAD, (int)sizeof(T), &m[f]))) return rc;
+        if ((rc = get_map(ps[f], g.nx, g.ny, g.pitch, tma::Geo<T>::BOXW, (int)sizeof(T), &m[f]))) return rc;
     const bool fast = a->mode == FKC_MODE_FAST;
     // reduction level: 0 none, 1 mass / maxima / error word, 2 + CFL bound
     const RedPtrs rp = to_red(a->red);

@@ -59,12 +59,26 @@ constexpr int R = FKC_TMA_R;             // rows per stage
 constexpr int S = FKC_TMA_S;             // ring stages per warp
 // T = float (4 cells per lane) or double (2 cells per lane): one 16-byte
 // vector per lane and row either way.
+#ifndef FKC_F64_CPL
+#define FKC_F64_CPL 2     // f64 cells per lane: 2 (one 16-B vector) or 1 (8 B lanes, half the register
+                          // window: 154-168 registers, 3 CTAs per SM -- correct, but measured 14 % slower
+                          // in fast mode, 9 % in exact: per-row overheads over half the cells)
+#endif
 template <class T> struct Geo {
-    static constexpr int CPL = 16 / (int)sizeof(T);       // cells per lane
+    static constexpr int CPL = sizeof(T) == 8 ? FKC_F64_CPL : 4;   // cells per lane
+    static constexpr int VEC = CPL * (int)sizeof(T);      // bytes per lane and row
+    static constexpr int LEAD = 16 / (int)sizeof(T) - 1;  // tensor column = full column + LEAD (fkc_sw.cu get_map)
     static constexpr int LOAD = 32 * CPL;                 // columns loaded per strip
     static constexpr int OWN = 30 * CPL;                  // columns owned per strip
-    static constexpr int FIELD_BYTES = R * LOAD * (int)sizeof(T);
+    // TMA box starts must be 16-B aligned.  With 16-B lanes every strip's
+    // first loaded column is; with 8-B lanes (f64, CPL 1) every other strip
+    // starts one column late, so the box takes 2 extra columns and the lanes
+    // read from column `shift` (0 or 1) of it.
+    static constexpr int BOXW = VEC == 16 ? LOAD : LOAD + 2;          // columns per TMA box
+    static constexpr int ROWB = BOXW * (int)sizeof(T);                // bytes per staged row
+    static constexpr int FIELD_BYTES = (R * ROWB + 127) / 128 * 128;  // 128-B aligned TMA destinations
     static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
+    static constexpr int TX_BYTES = 3 * R * ROWB;                     // bytes a stage's 3 boxes deliver
     static constexpr int WARP_RING = S * STAGE_BYTES;
     static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
     template <bool FAST, int RED = 0> static constexpr int ctas_per_sm() {
@@ -169,21 +183,26 @@ __device__ __forceinline__ VecF<T> lds_vec(uint32_t a) {
     if constexpr (sizeof(T) == 4)
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(a));
-    else
+    else if constexpr (tma::Geo<T>::CPL == 2)
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "r"(a));
+    else
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r.v[0]) : "r"(a));
     return r;
 }
 template <class T, int CPL>
 __device__ __forceinline__ void stg_vec(T* p, const T (&v)[CPL], T sgn = T(1)) {
     if constexpr (sizeof(T) == 4)
         *(float4*)p = make_float4(sgn * v[0], sgn * v[1], sgn * v[2], sgn * v[3]);
-    else
+    else if constexpr (CPL == 2)
         *(double2*)p = make_double2(sgn * v[0], sgn * v[1]);
+    else
+        *p = sgn * v[0];
 }
 // the new state's row store (evict-last with FKC_L2_HINTS)
 template <class T, int CPL>
 __device__ __forceinline__ void stg_row(T* p, const T (&v)[CPL]) {
 #if FKC_L2_HINTS
+    static_assert(sizeof(T) == 4 || CPL == 2, "L2 hints: 16-B vectors only");
     if constexpr (sizeof(T) == 4)
         asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
                      :: "l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(l2_policy_evict_last()) : "memory");
@@ -200,7 +219,7 @@ template <class T>
 __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUtensorMap* mH,
                                             const CUtensorMap* mU, const CUtensorMap* mV, int tx, int ty) {
     constexpr int FB = tma::Geo<T>::FIELD_BYTES;
-    mbar_expect_tx(bar, tma::Geo<T>::STAGE_BYTES);
+    mbar_expect_tx(bar, tma::Geo<T>::TX_BYTES);
     tma_load_2d(st, mH, tx, ty, bar);
     tma_load_2d(st + FB, mU, tx, ty, bar);
     tma_load_2d(st + 2 * FB, mV, tx, ty, bar);
@@ -296,7 +315,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * WARPS + warp;
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
-    const int tx = xs + CPL - 1;                         // its tensor column
+    const int txl = xs + G::LEAD;                        // its tensor column
+    const int tx = G::VEC == 16 ? txl : (txl & ~1);      // box start (16-B aligned)
     if (xs + CPL > nx) return;                           // strip owns nothing (ragged last band)
     int y0, nrows;                                       // first interior row of the segment, rows
     seg_rows(sm, blockIdx.y, ny, y0, nrows);
@@ -316,7 +336,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int ytop = y0 + nrows;                         // top loaded row (halo above the segment)
     auto stage_y = [&](int k) { return down ? ytop - k * R - (R - 1) : y0 - 1 + k * R; };
     const T vsign = down ? T(-1) : T(1);
-    const int row_bytes = down ? -(G::LOAD * (int)sizeof(T)) : G::LOAD * (int)sizeof(T);   // stage row step
+    const int row_bytes = down ? -G::ROWB : G::ROWB;    // stage row step
     const uint32_t ring = sbase + warp * G::WARP_RING;
     const uint32_t full = sbase + WARPS * G::WARP_RING + warp * tma::S * 8;
 
@@ -356,7 +376,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const bool any_bad = __any_sync(0xffffffffu, bad != 0);
     const bool edge_rows = (y0 == 1) || (y0 + nrows - 1 == ny);
     const bool edge_cols = owner && ((X == 1) || (X + CPL - 1 == nx));
-    const uint32_t lane_off = 16u * lane;
+    const uint32_t lane_off = (uint32_t)G::VEC * lane + (uint32_t)((txl - tx) * (int)sizeof(T));
 
     // the y-sweep's register window: packed-pair engine for f32 fast mode
     // (sw_pair.cuh), scalar engine otherwise
@@ -400,7 +420,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         }
         mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
         // first row of the stage in sweep order (boxes are stored bottom-up)
-        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * (G::LOAD * (int)sizeof(T)) : 0);
+        const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * G::ROWB : 0);
 #pragma unroll UNR
         for (int r = 0; r < R; ++r) {
             const int n = k * R + r;              // loaded row index; row y0-1+n (top-down: ytop-n)
