@@ -298,29 +298,54 @@ SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
     return m;
 }
 
-template <class T, bool FAST, int RED>
+template <class T, bool FAST, int RED, int NW>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
     using G = tma::Geo<T>;
-    auto kern = sw_step_tma<T, FAST, RED>;
+    using B = tma::Blk<T, NW>;
+    auto kern = sw_step_tma<T, FAST, RED, NW>;
     static std::once_flag attr_once;   // per instantiation; thread-safe
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM_BYTES);
     });
     if (attr_err != cudaSuccess)
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
     const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
-    const int nbands = (nstrips + tma::WARPS - 1) / tma::WARPS;
-    SegMap sm = pick_segmap(nbands, g.ny, G::template ctas_per_sm<FAST>());
+    const int nbands = (nstrips + NW - 1) / NW;
+    SegMap sm = pick_segmap(nbands, g.ny, B::template ctas_per_sm<FAST, RED>());
     sm.rev = next_rev(st);
     const int nseg = sm.tail == 0 ? (g.ny + sm.seg - 1) / sm.seg : sm.jt + (g.ny - sm.jt * sm.seg + sm.tail - 1) / sm.tail;
     dim3 grd(nbands, nseg);
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    launch_step(kern, grd, dim3(tma::THREADS), G::SMEM_BYTES, st, a->sync.counter == nullptr, m[0], m[1], m[2], g.nx, g.ny, g.pitch, sm, g_alt,
-                (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g, to_bcs(a->bc), to_red(a->red),
-                to_peers(a), to_sync(a));
+    launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, a->sync.counter == nullptr, m[0], m[1], m[2], g.nx,
+                g.ny, g.pitch, sm, g_alt, (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
+                to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
+}
+
+int g_warps = 0;   // warps per TMA CTA: 0 auto, else 1 / 2 / 4
+
+// Warps per CTA (B200 grid sweeps, profiles/r01/cta_warps.json): f32 fast
+// 1 below 2^25 cells (2896^2 179 -> 214, 4096^2 220 -> 229 Gcell/s), 4 above
+// (16384^2: 1 warp -1.7 %); f32 exact 2 (+2-4 % at 8192^2 .. 16384^2), 1
+// below 2^24 cells; f64 4.
+template <class T>
+int pick_warps(const fkc_grid& g, bool fast) {
+    if (g_warps) return g_warps;
+    if (sizeof(T) == 8) return 4;
+    const int64_t cells = (int64_t)g.nx * g.ny;
+    if (fast) return cells < (1LL << 25) ? 1 : 4;
+    return cells < (1LL << 24) ? 1 : 2;
+}
+
+template <class T, bool FAST, int RED>
+int launch_tma_nw(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
+    switch (pick_warps<T>(a->grid, FAST)) {
+        case 1: return launch_tma_t<T, FAST, RED, 1>(a, st, m);
+        case 2: return launch_tma_t<T, FAST, RED, 2>(a, st, m);
+        default: return launch_tma_t<T, FAST, RED, 4>(a, st, m);
+    }
 }
 
 template <class T>
@@ -336,11 +361,11 @@ int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
     const RedPtrs rp = to_red(a->red);
     const int lvl = rp.cfl_min ? 2 : (any_red(rp) ? 1 : 0);
     if (fast) {
-        if (lvl == 2) return launch_tma_t<T, true, 2>(a, st, m);
-        return lvl ? launch_tma_t<T, true, 1>(a, st, m) : launch_tma_t<T, true, 0>(a, st, m);
+        if (lvl == 2) return launch_tma_nw<T, true, 2>(a, st, m);
+        return lvl ? launch_tma_nw<T, true, 1>(a, st, m) : launch_tma_nw<T, true, 0>(a, st, m);
     }
-    if (lvl == 2) return launch_tma_t<T, false, 2>(a, st, m);
-    return lvl ? launch_tma_t<T, false, 1>(a, st, m) : launch_tma_t<T, false, 0>(a, st, m);
+    if (lvl == 2) return launch_tma_nw<T, false, 2>(a, st, m);
+    return lvl ? launch_tma_nw<T, false, 1>(a, st, m) : launch_tma_nw<T, false, 0>(a, st, m);
 }
 
 int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
@@ -385,6 +410,13 @@ int fkc_set_pdl(int on) {
 int fkc_set_tma_order(int mode) {
     if (mode < 0 || mode > 2) return fail(FKC_EUSAGE, "order must be 0, 1 or 2");
     g_rev_mode = mode;
+    return FKC_OK;
+}
+
+// test hook: warps per TMA CTA -- 0 auto, 1, 2 or 4
+int fkc_set_tma_warps(int nw) {
+    if (nw != 0 && nw != 1 && nw != 2 && nw != 4) return fail(FKC_EUSAGE, "warps per CTA must be 0 (auto), 1, 2 or 4");
+    g_warps = nw;
     return FKC_OK;
 }
 

@@ -36,7 +36,6 @@
 
 namespace fkc {
 namespace tma {
-constexpr int WARPS = 4;                 // warps (strips) per CTA
 #ifndef FKC_TMA_R
 #define FKC_TMA_R 4
 #endif
@@ -80,13 +79,24 @@ template <class T> struct Geo {
     static constexpr int STAGE_BYTES = 3 * FIELD_BYTES;
     static constexpr int TX_BYTES = 3 * R * ROWB;                     // bytes a stage's 3 boxes deliver
     static constexpr int WARP_RING = S * STAGE_BYTES;
-    static constexpr int SMEM_BYTES = WARPS * WARP_RING + WARPS * S * 8 + 128;
-    template <bool FAST, int RED = 0> static constexpr int ctas_per_sm() {
-        return sizeof(T) == 8 ? FKC_TMA_CTAS_F64 : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT);
+    // resident warps per SM (the FKC_TMA_CTAS_* macros count CTAs of 4 warps):
+    // f32 12 (<= 168 registers), f64 8
+    template <bool FAST, int RED = 0> static constexpr int warps_per_sm() {
+        return 4 * (sizeof(T) == 8 ? FKC_TMA_CTAS_F64
+                                   : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT));
     }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
-constexpr int THREADS = WARPS * 32;
+// A CTA of NW independent warps (strips): 1, 2 or 4 (host picks per size and
+// mode, fkc_sw.cu).  Smaller CTAs = finer scheduling granularity for the
+// hardware's CTA scheduler (shorter tail), larger = fewer CTA launches.
+template <class T, int NW> struct Blk {
+    static constexpr int THREADS = NW * 32;
+    static constexpr int SMEM_BYTES = NW * Geo<T>::WARP_RING + NW * S * 8 + 128;
+    template <bool FAST, int RED = 0> static constexpr int ctas_per_sm() {
+        return Geo<T>::template warps_per_sm<FAST, RED>() / NW;
+    }
+};
 #ifndef FKC_EXACT_ALWAYS_FIXUP
 #define FKC_EXACT_ALWAYS_FIXUP 0
 #endif
@@ -295,8 +305,8 @@ __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int
 // boxes: cell 1 is 128-B aligned).  Strip j owns columns
 // [1 + OWN j, OWN (j+1)] and loads full columns [1 + OWN j - CPL,
 // OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
-template <class T, bool FAST, int RED>
-__global__ void __launch_bounds__(tma::THREADS, tma::Geo<T>::template ctas_per_sm<FAST, RED>())
+template <class T, bool FAST, int RED, int NW>
+__global__ void __launch_bounds__(NW * 32, tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
             const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, SegMap sm, int alt,
             T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
@@ -313,7 +323,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * WARPS + warp;
+    const int strip = blockIdx.x * NW + warp;
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
     const int txl = xs + G::LEAD;                        // its tensor column
     const int tx = G::VEC == 16 ? txl : (txl & ~1);      // box start (16-B aligned)
@@ -338,7 +348,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const T vsign = down ? T(-1) : T(1);
     const int row_bytes = down ? -G::ROWB : G::ROWB;    // stage row step
     const uint32_t ring = sbase + warp * G::WARP_RING;
-    const uint32_t full = sbase + WARPS * G::WARP_RING + warp * tma::S * 8;
+    const uint32_t full = sbase + NW * G::WARP_RING + warp * tma::S * 8;
 
     // tile sides this warp exchanges with neighbour tiles (fused halo exchange)
     uint32_t sides = 0;

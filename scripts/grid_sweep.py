@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--sizes", default="128,256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--segs", default="0", help="comma list of TMA segment lengths to try (0 = auto)")
     ap.add_argument("--variants", default="auto", help="comma list of kernel variants (auto, tma, generic)")
+    ap.add_argument("--warps", default="0", help="comma list of warps per TMA CTA (0 auto, 1, 2, 4)")
     ap.add_argument("--orders", default="2", help="comma list of TMA segment orders (0 bottom-up, 2 alternating)")
     ap.add_argument("--pdl", default="1", help="comma list: programmatic dependent launch on (1) / off (0)")
     ap.add_argument("--tails", default="-1:1", help="comma list of guided-segmentation settings rows:waves (-1 auto, 0 off)")
@@ -38,10 +39,11 @@ def main():
     peak, _ = peaks()
     rows = []
     from paper_1107_2157_b200 import _native as N
-    todo = [(int(s), int(g), v, t, int(p), int(o)) for s in args.sizes.split(",") for g in args.segs.split(",")
+    todo = [(int(s), int(g), v, t, int(p), int(o), w) for s in args.sizes.split(",") for g in args.segs.split(",")
             for v in args.variants.split(",") for t in args.tails.split(",") for p in args.pdl.split(",")
-            for o in args.orders.split(",")]
-    for n, seg, variant, tail, pdl, order in todo:
+            for o in args.orders.split(",") for w in args.warps.split(",")]
+    for n, seg, variant, tail, pdl, order, warps in todo:
+        N.check(N.lib().fkc_set_tma_warps(int(warps)))
         N.check(N.lib().fkc_set_pdl(pdl))
         N.check(N.lib().fkc_set_tma_order(order))
         if variant == "generic" and seg:
@@ -74,7 +76,7 @@ def main():
             torch.cuda.synchronize()
             ms_eager = e0.elapsed_time(e1) / k
         g = n * n / (ms / 1e3) / 1e9
-        row = {"n": n, "seg": seg, "tail": tail, "pdl": pdl, "order": order, "variant": variant, "mode": args.mode, "ms_per_step_graph": round(ms, 5), "gcell_s": round(g, 2),
+        row = {"n": n, "seg": seg, "tail": tail, "pdl": pdl, "order": order, "warps": int(warps), "variant": variant, "mode": args.mode, "ms_per_step_graph": round(ms, 5), "gcell_s": round(g, 2),
                "hbm_gbs": round(24 * n * n / (ms / 1e3) / 1e9, 1), "frac_of_measured": round(24 * g / peak, 3),
                "ms_per_step_eager": round(ms_eager, 5),
                "regime": "L2-resident" if 6 * 4 * (n + 2) ** 2 <= 100e6 else "HBM",

@@ -45,6 +45,7 @@ def test_usage_errors_without_gpu():
     assert L.fkc_region_cpy(0, 16, 5, 5, 5, halo, 32, 5, None) == N.FKC_EDOMAIN  # HaloTooLarge
     assert L.fkc_set_tma_segment(-1) == N.FKC_EUSAGE
     assert L.fkc_set_pdl(2) == N.FKC_EUSAGE and L.fkc_set_tma_order(3) == N.FKC_EUSAGE
+    assert L.fkc_set_tma_warps(3) == N.FKC_EUSAGE
     assert L.fkc_set_tma_tail(-2, 1) == N.FKC_EUSAGE and L.fkc_set_tma_tail(4, 0) == N.FKC_EUSAGE
     # fused exchange: a peer line needs bc NONE on its side, and wait/signal come in pairs
     a.grid = N.Grid(8, 8, 12, 0, 0)
