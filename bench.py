@@ -199,6 +199,7 @@ def main():
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
                     help="field precision (f64: 48 B/cell; the headline is f32, BASELINE configs)")
     ap.add_argument("--seg", type=int, default=0, help="TMA kernel rows per CTA segment (0 = auto)")
+    ap.add_argument("--warps", type=int, default=0, choices=[0, 1, 2, 4], help="warps per TMA CTA (0 = auto)")
     ap.add_argument("--alt", type=int, default=1, choices=[0, 1],
                     help="TMA kernel: odd segments sweep top-down (L2 reuse of shared halo rows)")
     ap.add_argument("--transport", default="auto", choices=["auto", "peer", "nccl"],
@@ -254,6 +255,7 @@ def main():
     dev = torch.device("cuda", 0)
     if args.seg:
         N.check(N.lib().fkc_set_tma_segment(args.seg))
+    N.check(N.lib().fkc_set_tma_warps(args.warps))
     N.check(N.lib().fkc_set_tma_alternate(args.alt))
     st = device_gaussian_state(n, n, dev, precision=args.precision, amplitude=args.amplitude)
     dt0 = swdemo.stable_dt(st, 1.0)

@@ -326,22 +326,24 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
 
 int g_warps = 0;   // warps per TMA CTA: 0 auto, else 1 / 2 / 4
 
-// Warps per CTA (B200 grid sweeps, profiles/r01/cta_warps.json): f32 fast
-// 1 below 2^25 cells (2896^2 179 -> 214, 4096^2 220 -> 229 Gcell/s), 4 above
-// (16384^2: 1 warp -1.7 %); f32 exact 2 (+2-4 % at 8192^2 .. 16384^2), 1
-// below 2^24 cells; f64 4.
+// Warps per CTA (B200 sweeps, profiles/r01/cta_warps.json): f32 fast
+// without reductions 1 below 2^25 cells (2896^2 179 -> 214, 4096^2 219 ->
+// 229 Gcell/s), 4 above (16384^2: 1 warp -3 %); f32 fast with fused
+// reductions 1 (16384^2 diagnostics 244 -> 266, CFL 232 -> 252); f32 exact 1
+// below 2^24 cells, 2 above (16384^2 139 -> 148); f64 1 (fast 16384^2
+// 116 -> 131).
 template <class T>
-int pick_warps(const fkc_grid& g, bool fast) {
+int pick_warps(const fkc_grid& g, bool fast, int red) {
     if (g_warps) return g_warps;
-    if (sizeof(T) == 8) return 4;
+    if (sizeof(T) == 8) return 1;
     const int64_t cells = (int64_t)g.nx * g.ny;
-    if (fast) return cells < (1LL << 25) ? 1 : 4;
+    if (fast) return (red > 0 || cells < (1LL << 25)) ? 1 : 4;
     return cells < (1LL << 24) ? 1 : 2;
 }
 
 template <class T, bool FAST, int RED>
 int launch_tma_nw(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
-    switch (pick_warps<T>(a->grid, FAST)) {
+    switch (pick_warps<T>(a->grid, FAST, RED)) {
         case 1: return launch_tma_t<T, FAST, RED, 1>(a, st, m);
         case 2: return launch_tma_t<T, FAST, RED, 2>(a, st, m);
         default: return launch_tma_t<T, FAST, RED, 4>(a, st, m);
