@@ -455,11 +455,13 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (int rc = valid_peers(a)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     int variant = a->variant;
-    // AUTO: the TMA sweep for grids of >= 2^21 cells (HBM regime); below that
-    // (L2-resident / launch-bound) the generic kernel's one-thread-per-cell
-    // parallelism wins -- B200 grid sweep, profiles/r01/grid_sweep.json
+    // AUTO: the TMA sweep for grids of >= 1.25 Mi cells; below that (L2-
+    // resident, launch-bound) the generic kernel's one-thread-per-cell
+    // parallelism wins -- B200 sweep (profiles/r01/variant_crossover.json):
+    // 1024^2 generic 97 / 46 vs TMA 87 / 41 Gcell/s (fast / exact), 1448^2
+    // generic 107 / 44 vs TMA (1-warp CTAs) 132 / 67, crossing near 1216^2
     if (variant == FKC_VARIANT_AUTO)
-        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(1) << 21) ? FKC_VARIANT_TMA
+        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(5) << 18) ? FKC_VARIANT_TMA
                                                                                               : FKC_VARIANT_GENERIC;
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
