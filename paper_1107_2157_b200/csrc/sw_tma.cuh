@@ -363,6 +363,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncwarp();                                 // the barriers are initialised before any lane uses them
     pdl_wait();                                   // the previous step's output is complete
     if (lane == 0) {
         if (sides) peer_wait(sy, sides, red.err);   // before the first halo load

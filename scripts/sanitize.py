@@ -24,6 +24,11 @@ def main():
     from paper_1107_2157_b200.field import DeviceField, Field
 
     torch.cuda.set_device(0)
+    # optional overrides (isolating a sanitizer report): FKC_SAN_PDL=0|1, FKC_SAN_WARPS=0|1|2|4
+    if os.environ.get("FKC_SAN_PDL"):
+        N.check(N.lib().fkc_set_pdl(int(os.environ["FKC_SAN_PDL"])))
+    if os.environ.get("FKC_SAN_WARPS"):
+        N.check(N.lib().fkc_set_tma_warps(int(os.environ["FKC_SAN_WARPS"])))
     for prec in ("f32", "f64"):
         H, U, V = so.random_state(488, 70, prec, seed=3)
         st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, prec)) for a in (H, U, V)))
