@@ -242,6 +242,19 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
 int g_seg_override = 0;
 int g_alt = 1;   // alternate the sweep direction of odd segments (L2 reuse of shared halo rows)
 
+// SMs of the current device (148 on a B200), cached per device
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cached[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
@@ -250,7 +263,7 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     // take the longest of 32/24/16/12/8 rows that still gives >= 3 waves of
     // CTAs; on smaller grids the one whose CTAs fill the last wave best.
     const int cands[5] = {32, 24, 16, 12, 8};
-    const int64_t slots = 148LL * ctas_per_sm;
+    const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
     for (int seg : cands)
         if ((int64_t)nbands * ((ny + seg - 1) / seg) >= 3 * slots) return seg;
     int best = 8;
@@ -288,7 +301,7 @@ SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
     SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0, 0};
     int tail = g_tail_seg < 0 ? m.seg / 2 : g_tail_seg;
     if (tail <= 0 || tail >= m.seg || g_seg_override > 0) return m;
-    const int64_t slots = 148LL * ctas_per_sm;
+    const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
     // tail rows: enough segments to fill g_tail_waves waves of CTAs
     const int64_t tail_segs = (g_tail_waves * slots + nbands - 1) / nbands;
     const int64_t tail_rows = tail_segs * tail;
