@@ -258,15 +258,17 @@ int sm_count() {
 int pick_seg(int nbands, int ny, int ctas_per_sm) {
     if (g_seg_override > 0) return g_seg_override;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
-    // pipeline prologue; short ones shrink the tail of the last wave.  B200
-    // sweep (profiles/r01/seg_sweep2.json, fast mode, 2048^2 .. 16384^2):
-    // take the longest of 32/24/16/12/8 rows that still gives >= 3 waves of
-    // CTAs; on smaller grids the one whose CTAs fill the last wave best.
-    const int cands[5] = {32, 24, 16, 12, 8};
+    // pipeline prologue; short ones shrink the tail of the last wave.  A
+    // segment loads seg + 2 rows in stages of R = 4, so seg = 4k - 2 wastes
+    // no row of its last stage (1024^2: 6 rows 114 vs 8 rows 87 Gcell/s).
+    // B200 sweeps (profiles/r01/seg_sweep2.json, seg_sweep3.json): take the
+    // longest of 30/22/14/10/6 rows that still gives >= 3 waves of CTAs; on
+    // smaller grids the one whose CTAs fill the last wave best.
+    const int cands[5] = {30, 22, 14, 10, 6};
     const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
     for (int seg : cands)
         if ((int64_t)nbands * ((ny + seg - 1) / seg) >= 3 * slots) return seg;
-    int best = 8;
+    int best = 6;
     double best_fill = -1.0;
     for (int seg : cands) {
         const int64_t c = (int64_t)nbands * ((ny + seg - 1) / seg);
@@ -299,7 +301,8 @@ int g_tail_waves = 1;   // CTA waves of tail segments
 // segments of `tail` rows.
 SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
     SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0, 0};
-    int tail = g_tail_seg < 0 ? m.seg / 2 : g_tail_seg;
+    // auto: about half the segment, again 4k - 2 rows (30 -> 14, 22 -> 10, 14 -> 6, 10 / 6 -> 2)
+    int tail = g_tail_seg < 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : g_tail_seg;
     if (tail <= 0 || tail >= m.seg || g_seg_override > 0) return m;
     const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
     // tail rows: enough segments to fill g_tail_waves waves of CTAs
@@ -340,18 +343,17 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
 int g_warps = 0;   // warps per TMA CTA: 0 auto, else 1 / 2 / 4
 
 // Warps per CTA (B200 sweeps, profiles/r01/cta_warps.json): f32 fast
-// without reductions 1 below 2^25 cells (2896^2 179 -> 214, 4096^2 219 ->
-// 229 Gcell/s), 4 above (16384^2: 1 warp -3 %); f32 fast with fused
-// reductions 1 (16384^2 diagnostics 244 -> 266, CFL 232 -> 252); f32 exact 1
-// below 2^24 cells, 2 above (16384^2 139 -> 148); f64 1 (fast 16384^2
-// 116 -> 131).
+// without reductions 1 below 3*2^23 cells (2048^2: 186 vs 151 Gcell/s with
+// 4), 4 above (16384^2: 269 vs 262 with 1); f32 fast with fused reductions 1
+// (16384^2 diagnostics 244 -> 266, CFL 232 -> 252); f32 exact 1 below 2^26
+// cells, 2 above (16384^2 153 vs 150); f64 1 (fast 16384^2 116 -> 131).
 template <class T>
 int pick_warps(const fkc_grid& g, bool fast, int red) {
     if (g_warps) return g_warps;
     if (sizeof(T) == 8) return 1;
     const int64_t cells = (int64_t)g.nx * g.ny;
-    if (fast) return (red > 0 || cells < (1LL << 25)) ? 1 : 4;
-    return cells < (1LL << 24) ? 1 : 2;
+    if (fast) return (red > 0 || cells < (3LL << 23)) ? 1 : 4;
+    return cells < (1LL << 26) ? 1 : 2;
 }
 
 template <class T, bool FAST, int RED>
@@ -468,13 +470,13 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (int rc = valid_peers(a)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     int variant = a->variant;
-    // AUTO: the TMA sweep for grids of >= 1.25 Mi cells; below that (L2-
+    // AUTO: the TMA sweep for grids of >= 640 Ki cells; below that (L2-
     // resident, launch-bound) the generic kernel's one-thread-per-cell
     // parallelism wins -- B200 sweep (profiles/r01/variant_crossover.json):
-    // 1024^2 generic 97 / 46 vs TMA 87 / 41 Gcell/s (fast / exact), 1448^2
-    // generic 107 / 44 vs TMA (1-warp CTAs) 132 / 67, crossing near 1216^2
+    // 768^2 generic 85 / 43 vs TMA 43 (exact), 896^2 generic 92 / 45 vs TMA
+    // 96 / 60, 1024^2 generic 98 / 46 vs TMA 112 / 71 Gcell/s (fast / exact)
     if (variant == FKC_VARIANT_AUTO)
-        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(5) << 18) ? FKC_VARIANT_TMA
+        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(5) << 17) ? FKC_VARIANT_TMA
                                                                                               : FKC_VARIANT_GENERIC;
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
