@@ -314,6 +314,21 @@ SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
     return m;
 }
 
+// The TMA kernel's launch geometry: bands of NW strips x row segments.
+struct TmaPlan {
+    int nbands, nseg;
+    SegMap sm;
+};
+TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm) {
+    TmaPlan p;
+    const int nstrips = (nx + own - 1) / own;
+    p.nbands = (nstrips + nw - 1) / nw;
+    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm);
+    const SegMap& m = p.sm;
+    p.nseg = m.tail == 0 ? (ny + m.seg - 1) / m.seg : m.jt + (ny - m.jt * m.seg + m.tail - 1) / m.tail;
+    return p;
+}
+
 template <class T, bool FAST, int RED, int NW>
 int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
     using G = tma::Geo<T>;
@@ -327,12 +342,10 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     if (attr_err != cudaSuccess)
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
-    const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
-    const int nbands = (nstrips + NW - 1) / NW;
-    SegMap sm = pick_segmap(nbands, g.ny, B::template ctas_per_sm<FAST, RED>());
-    sm.rev = next_rev(st);
-    const int nseg = sm.tail == 0 ? (g.ny + sm.seg - 1) / sm.seg : sm.jt + (g.ny - sm.jt * sm.seg + sm.tail - 1) / sm.tail;
-    dim3 grd(nbands, nseg);
+    TmaPlan p = plan_tma(g.nx, g.ny, G::OWN, NW, B::template ctas_per_sm<FAST, RED>());
+    p.sm.rev = next_rev(st);
+    dim3 grd(p.nbands, p.nseg);
+    SegMap sm = p.sm;
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
     launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, a->sync.counter == nullptr, m[0], m[1], m[2], g.nx,
                 g.ny, g.pitch, sm, g_alt, (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
@@ -427,6 +440,26 @@ int fkc_set_pdl(int on) {
 int fkc_set_tma_order(int mode) {
     if (mode < 0 || mode > 2) return fail(FKC_EUSAGE, "order must be 0, 1 or 2");
     g_rev_mode = mode;
+    return FKC_OK;
+}
+
+// The TMA kernel's schedule for a grid (no device work; CPU-testable):
+// out[0..6] = warps per CTA, bands, row segments (grid.y), segment rows,
+// tail segment rows (0 = uniform), first tail segment, CTAs per SM.
+int fkc_tma_plan(const fkc_grid* g, int mode, int red_level, int* out) {
+    if (!g || !out || g->nx <= 0 || g->ny <= 0 || (g->dtype != FKC_F32 && g->dtype != FKC_F64) ||
+        (mode != FKC_MODE_EXACT && mode != FKC_MODE_FAST) || red_level < 0 || red_level > 2)
+        return fail(FKC_EUSAGE, "fkc_tma_plan: bad arguments");
+    const bool f32 = g->dtype == FKC_F32, fast = mode == FKC_MODE_FAST;
+    const int nw = f32 ? pick_warps<float>(*g, fast, red_level) : pick_warps<double>(*g, fast, red_level);
+    int wps;   // resident warps per SM of that instantiation
+    if (f32) wps = fast ? (red_level ? tma::Geo<float>::warps_per_sm<true, 1>() : tma::Geo<float>::warps_per_sm<true, 0>())
+                        : tma::Geo<float>::warps_per_sm<false, 0>();
+    else wps = tma::Geo<double>::warps_per_sm<true, 0>();
+    const int own = f32 ? tma::Geo<float>::OWN : tma::Geo<double>::OWN;
+    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw);
+    out[0] = nw; out[1] = p.nbands; out[2] = p.nseg; out[3] = p.sm.seg; out[4] = p.sm.tail; out[5] = p.sm.jt;
+    out[6] = wps / nw;
     return FKC_OK;
 }
 

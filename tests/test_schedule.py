@@ -1,0 +1,62 @@
+"""Host-side launch schedule of the TMA kernel (csrc/fkc_sw.cu plan_tma /
+pick_warps / pick_segmap), queried through fkc_tma_plan -- no GPU needed.
+The rules checked are the ones DESIGN.md section 5.1 states: segments of
+4k - 2 rows (no discarded rows in the last 4-row TMA stage), shorter tail
+segments launched last, >= 3 waves of CTAs where the grid allows it, the
+warps-per-CTA choice by size / mode / reductions / precision."""
+
+import ctypes
+
+import pytest
+
+from paper_1107_2157_b200 import _native as N
+
+SM = 148   # no device here: the library falls back to the B200's SM count
+
+
+def plan(n, mode="fast", red=0, prec="f32", ny=None):
+    g = N.Grid(n, ny or n, n + 32, N.F32 if prec == "f32" else N.F64, 0)
+    out = (ctypes.c_int * 7)()
+    N.check(N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if mode == "fast" else N.MODE_EXACT, red, out))
+    keys = ("warps", "bands", "nseg", "seg", "tail", "jt", "ctas_per_sm")
+    return dict(zip(keys, list(out)))
+
+
+@pytest.mark.parametrize("n", [900, 1024, 1448, 2048, 2896, 4096, 5792, 8192, 16384, 32768])
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+@pytest.mark.parametrize("red", [0, 1, 2])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_plan_rules(n, mode, red, prec):
+    p = plan(n, mode, red, prec)
+    assert p["warps"] in (1, 2, 4)
+    assert p["seg"] % 4 == 2, p                        # seg + 2 halo rows = whole 4-row stages
+    if p["tail"]:
+        assert p["tail"] % 4 == 2 and p["tail"] < p["seg"] and 0 < p["jt"] < p["nseg"], p
+        covered = p["jt"] * p["seg"] + (p["nseg"] - p["jt"]) * p["tail"]
+        assert n <= covered < n + p["tail"], (p, covered)
+    else:
+        assert n <= p["nseg"] * p["seg"] < n + p["seg"], p
+    cpl = 4 if prec == "f32" else 2
+    strips = -(-n // (30 * cpl))
+    assert p["bands"] == -(-strips // p["warps"])
+    if n >= 8192:                                      # large grids: at least 3 waves of CTAs
+        assert p["bands"] * p["nseg"] >= 3 * SM * p["ctas_per_sm"], p
+
+
+def test_plan_choices():
+    assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 30           # headline: 4-warp CTAs, 30-row segments
+    assert plan(16384, red=1)["warps"] == 1 and plan(16384, red=2)["warps"] == 1
+    assert plan(2048)["warps"] == 1 and plan(4096)["warps"] == 1
+    assert plan(16384, "exact")["warps"] == 2 and plan(4096, "exact")["warps"] == 1
+    assert plan(16384, prec="f64")["warps"] == 1
+    assert plan(16384)["ctas_per_sm"] * plan(16384)["warps"] == 12          # 12 resident warps per SM (f32)
+    assert plan(16384, prec="f64")["ctas_per_sm"] * plan(16384, prec="f64")["warps"] == 8
+
+
+def test_plan_usage_errors():
+    g = N.Grid(0, 16, 32, N.F32, 0)
+    out = (ctypes.c_int * 7)()
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 0, out) == N.FKC_EUSAGE
+    g = N.Grid(64, 16, 96, N.F32, 0)
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), 7, 0, out) == N.FKC_EUSAGE
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 3, out) == N.FKC_EUSAGE
