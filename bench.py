@@ -298,7 +298,8 @@ def main():
         "config": {"workload": workload(n, 1, args.precision),
                    "precision": args.precision, "diagnostics": args.diag,
                    "mode": args.mode, "parity": "bit-exact vs oracle" if args.mode == "exact" else FAST_PARITY,
-                   "variant": args.variant, "global_batch": cells, "parallelism": "single GPU",
+                   "variant": args.variant, "schedule": tma_schedule(n, args), "global_batch": cells,
+                   "parallelism": "single GPU",
                    "l2": f"working set {BYTES_PER_CELL[args.precision] * (n + 2) * (n + 2) / 1e9:.1f} GB >> "
                          "126 MB L2 (no flush needed)"},
         "hbm_gbs": round(achieved, 1),
@@ -322,6 +323,23 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line))
     return 0
+
+
+def tma_schedule(n, args):
+    """The TMA kernel's launch schedule for this run (fkc_tma_plan: the
+    host-side plan the library uses), or None for the generic kernel."""
+    import ctypes
+    from paper_1107_2157_b200 import _native as N
+    if args.variant == "generic" or (args.variant == "auto" and n * n < (5 << 17)):
+        return None
+    g = N.Grid(n, n, n + 32, N.F32 if args.precision == "f32" else N.F64, 0)
+    out = (ctypes.c_int * 7)()
+    red = {"none": 0, "diag": 1, "cfl": 2}[args.diag]
+    if N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if args.mode == "fast" else N.MODE_EXACT, red, out):
+        return None
+    w, bands, nseg, seg, tail, jt, cps = list(out)
+    return {"kernel": "sw_step_tma", "warps_per_cta": w, "ctas": bands * nseg, "ctas_per_sm": cps,
+            "segment_rows": seg, "tail_segment_rows": tail, "order": "alternating per step", "pdl": True}
 
 
 def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32", diag="none"):
