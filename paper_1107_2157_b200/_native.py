@@ -27,7 +27,7 @@ EXPORTS = (
     "fkc_sw_step", "fkc_sw_advance_n", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
     "fkc_ipc_export", "fkc_ipc_open", "fkc_ipc_close",
-    "fkc_set_tma_segment", "fkc_set_tma_tail", "fkc_set_tma_order", "fkc_set_tma_warps", "fkc_tma_plan", "fkc_set_pdl", "fkc_set_tma_alternate", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_last_error", "fkc_abi_version",
+    "fkc_set_tma_segment", "fkc_set_tma_tail", "fkc_set_tma_order", "fkc_set_tma_warps", "fkc_tma_plan", "fkc_set_pdl", "fkc_set_tma_alternate", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_test_sqrt2_f32", "fkc_last_error", "fkc_abi_version",
 )
 ABI_VERSION = 2
 
@@ -129,6 +129,7 @@ def lib():
         "fkc_set_tma_alternate": [ctypes.c_int],
         "fkc_test_div_f32": [vp, vp, vp, vp, i64, vp],
         "fkc_test_div_f64": [vp, vp, vp, vp, i64, vp],
+        "fkc_test_sqrt2_f32": [vp, vp, vp, i64, vp],
         "fkc_abi_version": [],
         "fkc_last_error": [],
     }

@@ -483,6 +483,12 @@ int fkc_test_div_f64(const double* a, const double* b, double* q, double* qref, 
     return check_launch("test_div64_kernel");
 }
 
+int fkc_test_sqrt2_f32(const float* x, float* s, float* sref, int64_t n, void* stream) {
+    if (!x || !s || !sref || n < 0 || (n & 1)) return fail(FKC_EUSAGE, "bad arguments (n must be even)");
+    test_sqrt2_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(x, s, sref, n);
+    return check_launch("test_sqrt2_kernel");
+}
+
 int fkc_test_div_f32(const float* a, const float* b, float* q, float* qref, int64_t n, void* stream) {
     if (!a || !b || !q || !qref || n < 0) return fail(FKC_EUSAGE, "bad arguments");
     test_div_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, b, q, qref, n);
