@@ -61,7 +61,7 @@ def peaks():
 class ClockSampler:
     """NVML sampling of SM clock and throttle reasons during the timed region."""
 
-    def __init__(self, index=0, period=0.02):
+    def __init__(self, index=0, period=0.004):
         self.samples, self.reasons = [], set()
         self.period, self.index = period, index
         self.ok = False
@@ -117,14 +117,19 @@ class ClockSampler:
 # CPU reference (oracle port) -- only used for the cpu_baseline / --impl reference legs
 # ---------------------------------------------------------------------------
 
-def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads=None, warmup=2):
-    """Time the C restatement of the reference CPU path (all host threads)
-    on a bounded slab n x rows of the same workload; `warmup` untimed steps
-    first (page faults of fresh buffers, thread start-up)."""
+def cpu_reference_run(n, steps, warmup, threads=None, budget_s=None):
+    """The reference CPU path of the step timed on the host cores: the C
+    restatement of the reference algorithm (oracle/sw_oracle.c, DSL op
+    order, all `threads` host threads) on the FULL n x n workload -- the
+    same grid, init and dt as the GPU arm.  `warmup` untimed steps (page
+    faults of the fresh buffers, thread start-up), then `steps` timed steps
+    (or as many as fit in `budget_s` seconds, at least 2); the per-step
+    median is reported.  Both CPU legs (our arm's cpu_baseline and
+    --impl reference) use this one function, so they measure the same thing."""
     from oracle import c_oracle
     from oracle import sw_oracle as so
     threads = threads or len(os.sched_getaffinity(0))
-    H, U, V = so.init_state(n, rows, "f32")
+    H, U, V = so.init_state(n, n, "f32")
     dt = 0.3 * so.stable_dt(H, U, V, 1.0, 1.0)
     a = (H, U, V)
     b = tuple(np.empty_like(x) for x in a)
@@ -133,16 +138,30 @@ def cpu_port_sample(n, rows, budget_s=12.0, min_steps=2, max_steps=1000, threads
         a, b = b, a
     times = []
     t_start = time.perf_counter()
-    while len(times) < max_steps and (len(times) < min_steps or time.perf_counter() - t_start < budget_s):
+    while len(times) < steps and (budget_s is None or len(times) < 2 or time.perf_counter() - t_start < budget_s):
         t0 = time.perf_counter()
         c_oracle.step(*a, 1.0, 1.0, dt, out=b, threads=threads)
         times.append(time.perf_counter() - t0)
         a, b = b, a
     med = statistics.median(times)
-    return {"value": n * rows / med / 1e9, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
-            "sample": f"C restatement of the reference step (oracle/sw_oracle.c, DSL op order) on a "
-                      f"{n}x{rows} slab of the {n}x{n} workload, median of {len(times)} steps, "
-                      f"{threads} threads", "ms_per_step": med * 1e3}
+    return {"value": n * n / med / 1e9, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+            "sample": f"C restatement of the reference step (oracle/sw_oracle.c, DSL op order, -O2, no FMA) "
+                      f"on the full {n}x{n} workload, {warmup} warm-up steps, median of {len(times)} timed steps, "
+                      f"{threads} host threads", "ms_per_step": med * 1e3, "steps_timed": len(times),
+            "warmup": warmup}
+
+
+def cpu_reference_subprocess(n, steps, warmup, budget_s=None):
+    """cpu_reference_run in a fresh interpreter (no CUDA context, no pinned
+    buffers, no torch threads): the same conditions as the --impl
+    reference arm, which the driver runs as its own process."""
+    import subprocess
+    code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench.cpu_reference_run(%d, %d, %d, budget_s=%r)))" % (ROOT, n, steps, warmup, budget_s))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-500:])
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 def numpy_sample(n, rows):
@@ -215,6 +234,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the other-mode timing (profiling runs)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the BASELINE config 2 (4096^2 x 1000 steps) and grid-sweep (config 5b) lines")
+    ap.add_argument("--sweep", default="128,256,512,1024,2048,4096,8192,16384",
+                    help="grid sizes of the config-5b sweep reported under extras")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -225,16 +248,15 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        rows = 1024
         cores = len(os.sched_getaffinity(0))
-        r = cpu_port_sample(n, rows, budget_s=1e9, min_steps=args.steps, max_steps=args.steps, threads=cores,
-                            warmup=args.warmup)
+        r = cpu_reference_run(n, args.steps, args.warmup, threads=cores)
         line = {"metric": METRIC, "value": r["value"], "unit": "Gcell-updates/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
-                "config": {"workload": workload(n, world), "parallelism": f"{cores} host threads",
-                           "sample": f"each step times a {n}x{rows} slab of the workload (same per-cell work)"},
+                "config": {"workload": workload(n, 1), "parallelism": f"{cores} host threads",
+                           "sample": f"the full {n}x{n} grid every step (same grid, init and dt as the GPU arm); "
+                                     "per-step median"},
                 "impl": "reference",
                 "cpu_baseline": {"value": r["value"], "unit": "Gcell-updates/s", "cores": cores,
                                  "kind": "port", "sample": r["sample"]},
@@ -245,23 +267,19 @@ def main():
 
     import torch
     if world > 1:
-        from paper_1107_2157_b200 import decomp
-        return decomp.bench_main(args, rank, world)
+        return multi_gpu_main(args, rank, world)
 
     from paper_1107_2157_b200 import _native as N
     from paper_1107_2157_b200 import swdemo
 
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
-    if args.seg:
-        N.check(N.lib().fkc_set_tma_segment(args.seg))
-    N.check(N.lib().fkc_set_tma_warps(args.warps))
-    N.check(N.lib().fkc_set_tma_alternate(args.alt))
+    tune = N.Tune(seg=args.seg, warps=args.warps, no_alternate=1 - args.alt)
     st = device_gaussian_state(n, n, dev, precision=args.precision, amplitude=args.amplitude)
     dt0 = swdemo.stable_dt(st, 1.0)
     dt = 0.3 * dt0
     r = time_steps(st, n, dt, args.mode, args.variant, args.steps, args.warmup, sample_clocks=True,
-                   precision=args.precision, diag=args.diag)
+                   precision=args.precision, diag=args.diag, tune=tune)
     total_ms, per_launch, clocks = r["total_ms"], r["per_launch"], r["clocks"]
     ms_step = total_ms / args.steps
     cells = n * n
@@ -314,9 +332,13 @@ def main():
 
     if not args.no_e2e and args.precision == "f32":
         line["e2e"] = e2e_run(n, dt, args, dev)
+    if not args.no_extras and args.precision == "f32" and n == 16384:
+        line["extras"] = extras_run(args, dev)
     if not args.no_cpu:
         try:
-            cb = cpu_port_sample(n, 1024)
+            # same function and policy as --impl reference (warm-up, full grid,
+            # per-step median), bounded to ~15 s of CPU work
+            cb = cpu_reference_subprocess(n, args.steps, args.warmup, budget_s=15.0)
             cb["numpy_1core"] = numpy_sample(n, 256)
             line["cpu_baseline"] = cb
         except Exception as e:  # pragma: no cover
@@ -335,14 +357,17 @@ def tma_schedule(n, args):
     g = N.Grid(n, n, n + 32, N.F32 if args.precision == "f32" else N.F64, 0)
     out = (ctypes.c_int * 7)()
     red = {"none": 0, "diag": 1, "cfl": 2}[args.diag]
-    if N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if args.mode == "fast" else N.MODE_EXACT, red, out):
+    tune = N.Tune(seg=args.seg, warps=args.warps)
+    if N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if args.mode == "fast" else N.MODE_EXACT, red,
+                            ctypes.byref(tune), out):
         return None
     w, bands, nseg, seg, tail, jt, cps = list(out)
     return {"kernel": "sw_step_tma", "warps_per_cta": w, "ctas": bands * nseg, "ctas_per_sm": cps,
             "segment_rows": seg, "tail_segment_rows": tail, "order": "alternating per step", "pdl": True}
 
 
-def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32", diag="none"):
+def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, precision="f32", diag="none",
+               tune=None):
     """K steps of the fused step kernel, CUDA events on the launching stream
     (one event pair per launch: the step kernel is the only launch)."""
     import torch
@@ -351,7 +376,7 @@ def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, pre
                           variant=variant, precision=precision, cfl_factor=0.3)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        sim = swdemo.Simulation(cfg, state=st, diagnostics=diag != "none", stream=stream)
+        sim = swdemo.Simulation(cfg, state=st, diagnostics=diag != "none", stream=stream, tune=tune)
         sim.advance(warmup)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
@@ -377,51 +402,258 @@ def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, pre
             "per_launch": [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)], "clocks": clocks}
 
 
+def extras_run(args, dev):
+    """BASELINE config 2 (4096^2, 1000 steps, one native call per mode, after
+    10 warm-up steps) and the config-5b grid sweep 128^2 .. 16384^2 (fast
+    mode; each size's steps replayed from one CUDA graph), device-timed with
+    CUDA events.  Reported beside the headline, not as it."""
+    import torch
+    from paper_1107_2157_b200 import swdemo
+    out = {}
+    c2 = {}
+    for mode in ("fast", "exact"):
+        st = device_gaussian_state(4096, 4096, dev)
+        dt = 0.3 * swdemo.stable_dt(st, 1.0)
+        cfg = swdemo.SWConfig(nx=4096, ny=4096, steps=1010, dt=dt, mode=mode)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+            sim.advance(10)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sim.advance(1000)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        assert bool(torch.isfinite(sim.state().H.data).all().item())
+        c2[mode] = {"value": round(4096 * 4096 * 1000 / (ms / 1e3) / 1e9, 2), "ms_total": round(ms, 3),
+                    "us_per_step": round(ms, 3)}
+        del sim, st
+    out["config2_4096sq_1000_steps"] = {"unit": "Gcell-updates/s", **c2,
+                                        "how": "one fkc_sw_advance_n call of 1000 steps, CUDA events"}
+    sweep = []
+    for n in (int(x) for x in args.sweep.split(",") if x):
+        st = device_gaussian_state(n, n, dev)
+        dt = 0.3 * swdemo.stable_dt(st, 1.0)
+        cfg = swdemo.SWConfig(nx=n, ny=n, dt=dt, mode="fast")
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+            k = 20 if n >= 8192 else 200
+            replay = sim.capture(k)
+            replay()
+            torch.cuda.synchronize()
+            reps = max(2, min(50, int(1e9 / (n * n * k))))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / (reps * k)
+        sweep.append({"n": n, "us_per_step": round(ms * 1e3, 3), "value": round(n * n / (ms / 1e3) / 1e9, 2),
+                      "hbm_equiv_gbs": round(24 * n * n / (ms / 1e3) / 1e9, 1),
+                      "regime": "launch-bound" if n <= 512 else ("L2-resident" if n <= 2048 else "HBM")})
+        del sim, st
+        torch.cuda.empty_cache()
+    out["sweep_fast"] = {"unit": "Gcell-updates/s", "rows": sweep,
+                         "how": "Simulation.capture(k) CUDA graph replays, CUDA events, fixed dt"}
+    return out
+
+
 def e2e_run(n, dt, args, dev):
-    """Same metric through the public API with HOST buffers: the initial
-    state is copied from pinned host memory, ``swdemo.run`` advances it with
-    per-step fused diagnostics (mass, max|hu|, max|hv|, error word), and the
-    final state plus the per-step diagnostics come back to the host."""
+    """Same metric through the public API with HOST buffers, at the
+    commanded --steps: the initial state is copied from pinned host memory,
+    ``swdemo.run`` advances it with per-step fused diagnostics (mass,
+    max|hu|, max|hv|, error word; each step's row streamed back), and the
+    final state comes back to pinned host memory -- all inside the timed
+    region.  One untimed run of the same call first (a warm process: CUDA
+    context, allocator, tensor maps), then one timed run; a labelled
+    200-step run is reported beside it (the copies amortised over more
+    steps)."""
     import torch
     from paper_1107_2157_b200 import swdemo
     from paper_1107_2157_b200.field import Field
     from paper_1107_2157_b200.region import Extent
-    steps = max(args.steps, 200)
     st = device_gaussian_state(n, n, dev)
-    st2 = device_gaussian_state(n, n, dev)
     full = Extent(n + 2, n + 2)
     pinned = []
     for f in (st.H, st.U, st.V):
         t = torch.empty((n + 2, n + 2), dtype=torch.float32, pin_memory=True)
         t.copy_(f.data)
         pinned.append(t)
-    # their device blocks (input + output state) stay in torch's caching
-    # allocator and run() reuses them: a warm process (a first run that has
-    # to cudaMalloc 6 x 1.07 GB measured ~190 ms slower)
-    del st, st2
+    del st
+    torch.cuda.empty_cache()
     host_state = swdemo.SWState(*(Field(full, t.numpy(), "f32") for t in pinned))
     out_pinned = [torch.empty((n + 2, n + 2), dtype=torch.float32, pin_memory=True) for _ in range(3)]
     host_out = swdemo.SWState(*(Field(full, t.numpy(), "f32") for t in out_pinned))
-    cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps, dt=dt, mode=args.mode, variant=args.variant)
-    # two complete runs, the faster one reported (both listed): host-side
-    # noise on the shared box (PCIe copies, the launching thread) has been
-    # seen to halve a single run
-    runs = []
-    for _ in range(2):
+
+    def timed(steps):
+        cfg = swdemo.SWConfig(nx=n, ny=n, steps=steps, dt=dt, mode=args.mode, variant=args.variant)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = swdemo.run(cfg, state=host_state, out=host_out)
-        t1 = time.perf_counter()
-        runs.append(round(n * n * steps / (t1 - t0) / 1e9, 3))
+        el = time.perf_counter() - t0
+        return n * n * steps / el / 1e9, el, res
+
+    timed(min(args.steps, 3))                     # warm-up call (untimed)
+    value, el, res = timed(args.steps)
+    long_value, long_el, _ = timed(200)
     state_bytes = 3 * 4 * (n + 2) * (n + 2)
-    return {"value": max(runs), "runs": runs, "unit": "Gcell-updates/s",
-            "h2d_bytes_per_step": round(state_bytes / steps, 1),
-            "d2h_bytes_per_step": round((state_bytes + 40 * (steps + 1)) / steps, 1),
-            "steps": steps, "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
+    return {"value": round(value, 3), "unit": "Gcell-updates/s", "steps": args.steps,
+            "seconds": round(el, 4),
+            "h2d_bytes_per_step": round(state_bytes / args.steps, 1),
+            "d2h_bytes_per_step": round((state_bytes + 40 * (args.steps + 1)) / args.steps, 1),
+            "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
             "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel, each step's "
                            "40-byte row copied device->host after the step",
-            "allocator": "warm (device blocks of two setup states cached by torch and reused by run())",
-            "final_mass": res.rows[-1][3]}
+            "warm": "one untimed run() of the same call first (CUDA context, allocator, tensor maps)",
+            "final_mass": res.rows[-1][3],
+            "long_run_200_steps": {"value": round(long_value, 3), "seconds": round(long_el, 4),
+                                   "note": "same call with steps=200 (host copies amortised over 10x the steps)"}}
+
+
+# ---------------------------------------------------------------------------
+# N > 1 (torchrun): weak scaling 16384^2 cells per GPU, or strong scaling
+# ---------------------------------------------------------------------------
+
+def multi_gpu_main(args, rank: int, world: int) -> int:
+    """N > 1 (torchrun, one process per GPU): the decomposed run of
+    paper_1107_2157_b200.decomp -- weak scaling (BASELINE config 5) or, with
+    --global-n, strong scaling (config 4)."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.decomp import CartGrid, DistributedSimulation, choose_grid, gaussian_tile
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    # FKC_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo host collectives
+    # -- exercises the N>1 code path (IPC peer memory, mailboxes) on a
+    # one-GPU box; its timings are meaningless (time-sliced contexts)
+    one_dev = os.environ.get("FKC_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if one_dev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    px, py = choose_grid(world)
+    n = args.n
+    strong = bool(getattr(args, "global_n", 0))
+    # weak scaling (default): n^2 cells per GPU; strong: a fixed global grid
+    grid = CartGrid(px, py, args.global_n, args.global_n, "reflective") if strong else \
+        CartGrid(px, py, px * n, py * n, "reflective")
+    # fixed dt = 0.3 * stable_dt of the initial global state (h max 1.4, u = v = 0)
+    dt = 0.3 * 1.0 / float(np.sqrt(np.float32(9.8) * np.float32(1.4)))
+    cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport)
+        sim.advance(args.warmup)
+        torch.cuda.synchronize()
+        dist.barrier()
+        clocks = ClockSampler(local) if rank == 0 else None
+        if clocks:
+            clocks.__enter__()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        sim.advance(args.steps)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.__exit__(None, None, None)
+        dist.barrier()
+    ms = torch.tensor([t0.elapsed_time(t1)], device="cpu" if one_dev else dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    launches = sim._launches_per_step()
+    transport, fallback = sim.transport, sim.fallback_reason
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    e2e = None if getattr(args, "no_e2e", False) else multi_gpu_e2e(args, cfg, grid, rank, world, dev, one_dev)
+    cells = grid.NX * grid.NY
+    value = cells * args.steps / (total_ms / 1e3) / 1e9
+    if rank == 0:
+        peak, src = peaks()
+        per_gpu_gbs = BYTES_PER_CELL["f32"] * (cells / world) * args.steps / (total_ms / 1e3) / 1e9
+        line = {"metric": METRIC, "value": round(value, 3),
+                "unit": "Gcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+                "scaling": "strong" if strong else "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
+                "config": {"workload": (f"shallow-water {grid.NX}x{grid.NY} fp32 2-D decomposed {px}x{py}, "
+                                        "reflective, fixed dt=0.3*stable_dt (BASELINE config 4, strong scaling)")
+                           if strong else workload(n, world),
+                           "exchange": "one-cell halo exchange per step " +
+                                       ("fused into the step kernel (NVLink peer stores + mailbox flags)"
+                                        if transport == "peer" else "(pack + NCCL send/recv + unpack)"),
+
+                           "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
+                "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
+                             "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
+                             "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
+                "gpu_launches": args.steps * launches,
+                "clocks": clocks.summary()}
+        if e2e is not None:
+            line["e2e"] = e2e
+        line["config"]["transport"] = transport
+        if fallback:
+            line["config"]["transport_fallback"] = fallback[:300]
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
+def multi_gpu_e2e(args, cfg, grid, rank: int, world: int, dev, one_dev: bool):
+    """End to end through the public API at N GPUs: every rank's tile
+    starts in pinned host memory, DistributedSimulation uploads it, sets up
+    the exchange, advances `steps` steps and the final tile is copied back;
+    wall clock between two barriers, max over ranks."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.decomp import DistributedSimulation, gaussian_tile
+    from paper_1107_2157_b200.field import Field
+    from paper_1107_2157_b200.region import Extent
+    t = grid.tile(rank)
+    full = Extent(t.nx + 2, t.ny + 2)
+    steps = args.steps
+    pin = [torch.zeros((t.ny + 2, t.nx + 2), dtype=torch.float32, pin_memory=True) for _ in range(6)]
+    pin[0][1:-1, 1:-1] = torch.from_numpy(gaussian_tile(grid, rank, "f32", cfg.dx, cfg.dy, cfg.base,
+                                                        cfg.amplitude, cfg.center, cfg.width))
+    host_in = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[:3]), cfg.g, cfg.dx, cfg.dy)
+    host_out = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[3:]), cfg.g, cfg.dx, cfg.dy)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport, state=host_in)
+        sim.advance(steps)
+        sim.state().to_host(host_out)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    sim.close()
+    dist.barrier()
+    tt = torch.tensor([el], dtype=torch.float64, device="cpu" if one_dev else dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    el = float(tt.item())
+    state_bytes = 3 * 4 * (t.nx + 2) * (t.ny + 2) * world
+    return {"value": round(grid.NX * grid.NY * steps / el / 1e9, 3), "unit": "Gcell-updates/s",
+            "h2d_bytes_per_step": round(state_bytes / steps, 1), "d2h_bytes_per_step": round(state_bytes / steps, 1),
+            "steps": steps, "api": "DistributedSimulation(cfg, grid, rank, state=<host pinned tile>) -> "
+                                   "advance(steps) -> state().to_host(<host pinned tile>)"}
 
 
 if __name__ == "__main__":

@@ -21,15 +21,16 @@ F32, F64 = 0, 1
 BC_REFLECTIVE, BC_PERIODIC, BC_NONE = 0, 1, 2
 MODE_EXACT, MODE_FAST = 0, 1
 VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA = 0, 1, 2
-ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG = 1, 2, 4
+ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG, ERR_NONPOSITIVE_FACE = 1, 2, 4, 8
 
 EXPORTS = (
     "fkc_sw_step", "fkc_sw_advance_n", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
     "fkc_ipc_export", "fkc_ipc_open", "fkc_ipc_close",
-    "fkc_set_tma_segment", "fkc_set_tma_tail", "fkc_set_tma_order", "fkc_set_tma_warps", "fkc_tma_plan", "fkc_set_pdl", "fkc_set_tma_alternate", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_test_sqrt2_f32", "fkc_last_error", "fkc_abi_version",
+    "fkc_tma_plan", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_test_sqrt2_f32", "fkc_last_error",
+    "fkc_abi_version",
 )
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class NativeUnavailable(RuntimeError):
@@ -37,9 +38,19 @@ class NativeUnavailable(RuntimeError):
 
 
 class FkcError(RuntimeError):
+    """A non-zero C-ABI return code: 1 domain, 3 CUDA (2, usage, raises
+    :class:`FkcUsageError`)."""
+
     def __init__(self, code: int, msg: str):
         super().__init__(f"[fkc rc={code}] {msg}")
         self.code = code
+
+
+class FkcUsageError(FkcError, ValueError):
+    """FKC_EUSAGE: the call was rejected before touching device memory (bad
+    shape, pitch, alignment, pointer or enum).  ``swdemo.LaunchError``
+    derives from it, so callers of the reference API that catch
+    ``LaunchError`` / ``ValueError`` see these."""
 
 
 class Grid(ctypes.Structure):
@@ -64,6 +75,22 @@ class Sync(ctypes.Structure):
                 ("counter", ctypes.c_void_p), ("epoch", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
 
 
+class Tune(ctypes.Structure):
+    """fkc_sw_tune: per-call launch schedule (all zero = the defaults; results
+    never depend on it)."""
+    _fields_ = [("seg", ctypes.c_int32), ("tail_rows", ctypes.c_int32), ("tail_waves", ctypes.c_int32),
+                ("order", ctypes.c_int32), ("parity", ctypes.c_int32), ("warps", ctypes.c_int32),
+                ("no_pdl", ctypes.c_int32), ("no_alternate", ctypes.c_int32)]
+
+    def __init__(self, **kw):
+        super().__init__()
+        for k, v in kw.items():
+            setattr(self, k, int(v))
+
+    def copy(self) -> "Tune":
+        return Tune(**{k: getattr(self, k) for k, _ in self._fields_})
+
+
 class StepArgs(ctypes.Structure):
     _fields_ = [("grid", Grid),
                 ("H", ctypes.c_void_p), ("U", ctypes.c_void_p), ("V", ctypes.c_void_p),
@@ -72,7 +99,7 @@ class StepArgs(ctypes.Structure):
                 ("g", ctypes.c_double),
                 ("dt_bound", ctypes.c_void_p), ("cfl", ctypes.c_double),
                 ("bc", ctypes.c_int32 * 4), ("mode", ctypes.c_int32), ("variant", ctypes.c_int32),
-                ("red", Reduce), ("peer", PeerLine * 4), ("sync", Sync)]
+                ("red", Reduce), ("peer", PeerLine * 4), ("sync", Sync), ("tune", Tune)]
 
 
 class LoopArgs(ctypes.Structure):
@@ -120,13 +147,8 @@ def lib():
         "fkc_ipc_export": [vp, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(i64)],
         "fkc_ipc_open": [ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(vp)],
         "fkc_ipc_close": [vp],
-        "fkc_set_tma_segment": [ctypes.c_int],
-        "fkc_set_tma_tail": [ctypes.c_int, ctypes.c_int],
-        "fkc_set_pdl": [ctypes.c_int],
-        "fkc_set_tma_order": [ctypes.c_int],
-        "fkc_set_tma_warps": [ctypes.c_int],
-        "fkc_tma_plan": [ctypes.POINTER(Grid), ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
-        "fkc_set_tma_alternate": [ctypes.c_int],
+        "fkc_tma_plan": [ctypes.POINTER(Grid), ctypes.c_int, ctypes.c_int, ctypes.POINTER(Tune),
+                         ctypes.POINTER(ctypes.c_int)],
         "fkc_test_div_f32": [vp, vp, vp, vp, i64, vp],
         "fkc_test_div_f64": [vp, vp, vp, vp, i64, vp],
         "fkc_test_sqrt2_f32": [vp, vp, vp, i64, vp],
@@ -163,6 +185,9 @@ def ipc_close(base: int):
 def check(rc: int):
     if rc != FKC_OK:
         msg = lib().fkc_last_error().decode(errors="replace")
+        if rc == FKC_EUSAGE:
+            from .swdemo import LaunchError
+            raise LaunchError(rc, msg)
         raise FkcError(rc, msg)
 
 

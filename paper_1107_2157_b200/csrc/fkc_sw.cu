@@ -8,7 +8,6 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
-#include <unordered_map>
 #include <vector>
 #include <string>
 
@@ -106,6 +105,18 @@ int valid_peers(const fkc_sw_step_args* a) {
     return FKC_OK;
 }
 
+int valid_tune(const fkc_sw_tune& t) {
+    if (t.seg < 0) return fail(FKC_EUSAGE, "tune.seg must be >= 0");
+    if (t.tail_rows < -1) return fail(FKC_EUSAGE, "tune.tail_rows must be >= -1");
+    if (t.tail_waves < 0 || t.tail_waves > 64) return fail(FKC_EUSAGE, "tune.tail_waves must be in 0..64");
+    if (t.order < 0 || t.order > 2) return fail(FKC_EUSAGE, "tune.order must be 0, 1 or 2");
+    if (t.parity != 0 && t.parity != 1) return fail(FKC_EUSAGE, "tune.parity must be 0 or 1");
+    if (t.warps != 0 && t.warps != 1 && t.warps != 2 && t.warps != 4)
+        return fail(FKC_EUSAGE, "tune.warps must be 0 (auto), 1, 2 or 4");
+    if ((t.no_pdl | t.no_alternate) & ~1) return fail(FKC_EUSAGE, "tune.no_pdl / no_alternate must be 0 or 1");
+    return FKC_OK;
+}
+
 bool peers_tma_ok(const fkc_sw_step_args* a, int es) {
     for (int s = 2; s < 4; ++s)
         for (int f = 0; f < 3; ++f)
@@ -194,8 +205,6 @@ bool tma_eligible(const fkc_sw_step_args* a) {
     return peers_tma_ok(a, es);
 }
 
-int g_pdl = 1;   // launch the step kernels with programmatic stream serialisation
-
 // Launch with programmatic dependent launch (see pdl_wait in sw_kernels.cuh).
 // `pdl` false: plain launch -- for grids below ~512^2 (B200, CUDA graphs: the
 // programmatic edge costs more than it hides, 256^2 fast 26 -> 20 Gcell/s)
@@ -212,7 +221,7 @@ void launch_step(void (*kern)(KArgs...), dim3 grd, dim3 blk, size_t smem, cudaSt
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (g_pdl && pdl) ? 1 : 0;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -225,7 +234,7 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     dim3 grd((g.nx + 63) / 64, (g.ny + 3) / 4);
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(red);
-    const bool pdl = (int64_t)g.nx * g.ny >= (1 << 18) && a->sync.counter == nullptr;
+    const bool pdl = !a->tune.no_pdl && (int64_t)g.nx * g.ny >= (1 << 18) && a->sync.counter == nullptr;
 #define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
                  (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red, to_peers(a), to_sync(a)
     if (fast) {
@@ -238,9 +247,6 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
 #undef GEN_ARGS
     return check_launch("sw_step_generic");
 }
-
-int g_seg_override = 0;
-int g_alt = 1;   // alternate the sweep direction of odd segments (L2 reuse of shared halo rows)
 
 // SMs of the current device (148 on a B200), cached per device
 int sm_count() {
@@ -255,8 +261,8 @@ int sm_count() {
     return cached[dev];
 }
 
-int pick_seg(int nbands, int ny, int ctas_per_sm) {
-    if (g_seg_override > 0) return g_seg_override;
+int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
+    if (t.seg > 0) return t.seg;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
     // pipeline prologue; short ones shrink the tail of the last wave.  A
     // segment loads seg + 2 rows in stages of R = 4, so seg = 4k - 2 wastes
@@ -278,35 +284,27 @@ int pick_seg(int nbands, int ny, int ctas_per_sm) {
     return best;
 }
 
-int g_rev_mode = 2;     // segment order: 0 bottom-up, 1 top-down, 2 alternate per launch on a stream
-std::mutex g_rev_mu;
-std::unordered_map<cudaStream_t, int> g_rev;
-
-// Alternate the segment order per launch on a stream, so each step starts
-// with the rows its predecessor wrote last (still in L2).  Evaluated on the
-// host at launch (or capture) time; a captured graph of an even number of
-// steps keeps alternating across replays.
-int next_rev(cudaStream_t st) {
-    if (g_rev_mode != 2) return g_rev_mode;
-    std::lock_guard<std::mutex> lk(g_rev_mu);
-    int& r = g_rev[st];
-    r ^= 1;
-    return r;
+// Segment order: alternate per step (tune.parity, the global step index's
+// parity in fkc_sw_advance_n), so each step starts with the rows its
+// predecessor wrote last (still in L2).  Carried in the argument block, so
+// concurrent callers, streams and captured graphs never share state.
+int seg_rev(const fkc_sw_tune& t) {
+    if (t.order == 1) return 0;
+    if (t.order == 2) return 1;
+    return t.parity & 1;
 }
 
-int g_tail_seg = -1;    // tail segment rows (-1 auto, 0 off)
-int g_tail_waves = 1;   // CTA waves of tail segments
-
-// Guided segmentation: the last ~g_tail_waves waves of CTAs get short
+// Guided segmentation: the last ~tail_waves waves of CTAs get short
 // segments of `tail` rows.
-SegMap pick_segmap(int nbands, int ny, int ctas_per_sm) {
-    SegMap m{pick_seg(nbands, ny, ctas_per_sm), 0, 0, 0};
+SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t), 0, 0, 0};
     // auto: about half the segment, again 4k - 2 rows (30 -> 14, 22 -> 10, 14 -> 6, 10 / 6 -> 2)
-    int tail = g_tail_seg < 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : g_tail_seg;
-    if (tail <= 0 || tail >= m.seg || g_seg_override > 0) return m;
+    const int tail = t.tail_rows == 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : t.tail_rows;
+    if (tail <= 0 || tail >= m.seg || t.seg > 0) return m;
+    const int waves = t.tail_waves > 0 ? t.tail_waves : 1;
     const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
-    // tail rows: enough segments to fill g_tail_waves waves of CTAs
-    const int64_t tail_segs = (g_tail_waves * slots + nbands - 1) / nbands;
+    // tail rows: enough segments to fill `waves` waves of CTAs
+    const int64_t tail_segs = (waves * slots + nbands - 1) / nbands;
     const int64_t tail_rows = tail_segs * tail;
     if (tail_rows >= ny / 2) return m;   // small grid: keep it uniform
     m.jt = (int)((ny - tail_rows) / m.seg);
@@ -319,11 +317,11 @@ struct TmaPlan {
     int nbands, nseg;
     SegMap sm;
 };
-TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm) {
+TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t) {
     TmaPlan p;
     const int nstrips = (nx + own - 1) / own;
     p.nbands = (nstrips + nw - 1) / nw;
-    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm);
+    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm, t);
     const SegMap& m = p.sm;
     p.nseg = m.tail == 0 ? (ny + m.seg - 1) / m.seg : m.jt + (ny - m.jt * m.seg + m.tail - 1) / m.tail;
     return p;
@@ -342,18 +340,17 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     if (attr_err != cudaSuccess)
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
-    TmaPlan p = plan_tma(g.nx, g.ny, G::OWN, NW, B::template ctas_per_sm<FAST, RED>());
-    p.sm.rev = next_rev(st);
+    TmaPlan p = plan_tma(g.nx, g.ny, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune);
+    p.sm.rev = seg_rev(a->tune);
     dim3 grd(p.nbands, p.nseg);
     SegMap sm = p.sm;
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, a->sync.counter == nullptr, m[0], m[1], m[2], g.nx,
-                g.ny, g.pitch, sm, g_alt, (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
+    const bool pdl = !a->tune.no_pdl && a->sync.counter == nullptr;
+    launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, pdl, m[0], m[1], m[2], g.nx,
+                g.ny, g.pitch, sm, a->tune.no_alternate ? 0 : 1, (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
                 to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));
     return check_launch("sw_step_tma");
 }
-
-int g_warps = 0;   // warps per TMA CTA: 0 auto, else 1 / 2 / 4
 
 // Warps per CTA (B200 sweeps, profiles/r01/cta_warps.json): f32 fast
 // without reductions 1 below 3*2^23 cells (2048^2: 186 vs 151 Gcell/s with
@@ -361,8 +358,8 @@ int g_warps = 0;   // warps per TMA CTA: 0 auto, else 1 / 2 / 4
 // (16384^2 diagnostics 244 -> 266, CFL 232 -> 252); f32 exact 1 below 2^26
 // cells, 2 above (16384^2 153 vs 150); f64 1 (fast 16384^2 116 -> 131).
 template <class T>
-int pick_warps(const fkc_grid& g, bool fast, int red) {
-    if (g_warps) return g_warps;
+int pick_warps(const fkc_grid& g, bool fast, int red, const fkc_sw_tune& t) {
+    if (t.warps) return t.warps;
     if (sizeof(T) == 8) return 1;
     const int64_t cells = (int64_t)g.nx * g.ny;
     if (fast) return (red > 0 || cells < (3LL << 23)) ? 1 : 4;
@@ -371,7 +368,7 @@ int pick_warps(const fkc_grid& g, bool fast, int red) {
 
 template <class T, bool FAST, int RED>
 int launch_tma_nw(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
-    switch (pick_warps<T>(a->grid, FAST, RED)) {
+    switch (pick_warps<T>(a->grid, FAST, RED, a->tune)) {
         case 1: return launch_tma_t<T, FAST, RED, 1>(a, st, m);
         case 2: return launch_tma_t<T, FAST, RED, 2>(a, st, m);
         default: return launch_tma_t<T, FAST, RED, 4>(a, st, m);
@@ -412,68 +409,25 @@ extern "C" {
 const char* fkc_last_error(void) { return g_err.c_str(); }
 int fkc_abi_version(void) { return FKC_ABI_VERSION; }
 
-// test hook: force the row-segment length of the TMA kernel (0 = auto)
-int fkc_set_tma_segment(int seg) {
-    if (seg < 0) return fail(FKC_EUSAGE, "segment must be >= 0");
-    g_seg_override = seg;
-    return FKC_OK;
-}
-
-// test hook: guided segmentation -- tail segment rows (-1 auto = half the
-// segment, 0 off) and how many CTA waves of them
-int fkc_set_tma_tail(int rows, int waves) {
-    if (rows < -1 || waves < 1 || waves > 64) return fail(FKC_EUSAGE, "tail rows must be >= -1 and waves in 1..64");
-    g_tail_seg = rows;
-    g_tail_waves = waves;
-    return FKC_OK;
-}
-
-// test hook: programmatic dependent launch of the step kernels (1, default) or plain launches (0)
-int fkc_set_pdl(int on) {
-    if (on != 0 && on != 1) return fail(FKC_EUSAGE, "pdl must be 0 or 1");
-    g_pdl = on;
-    return FKC_OK;
-}
-
-// test hook: order of the TMA kernel's row segments -- 0 bottom-up, 1
-// top-down, 2 alternating per launch on a stream (default)
-int fkc_set_tma_order(int mode) {
-    if (mode < 0 || mode > 2) return fail(FKC_EUSAGE, "order must be 0, 1 or 2");
-    g_rev_mode = mode;
-    return FKC_OK;
-}
-
 // The TMA kernel's schedule for a grid (no device work; CPU-testable):
 // out[0..6] = warps per CTA, bands, row segments (grid.y), segment rows,
 // tail segment rows (0 = uniform), first tail segment, CTAs per SM.
-int fkc_tma_plan(const fkc_grid* g, int mode, int red_level, int* out) {
+int fkc_tma_plan(const fkc_grid* g, int mode, int red_level, const fkc_sw_tune* tune, int* out) {
     if (!g || !out || g->nx <= 0 || g->ny <= 0 || (g->dtype != FKC_F32 && g->dtype != FKC_F64) ||
         (mode != FKC_MODE_EXACT && mode != FKC_MODE_FAST) || red_level < 0 || red_level > 2)
         return fail(FKC_EUSAGE, "fkc_tma_plan: bad arguments");
+    const fkc_sw_tune t = tune ? *tune : fkc_sw_tune{};
+    if (int rc = valid_tune(t)) return rc;
     const bool f32 = g->dtype == FKC_F32, fast = mode == FKC_MODE_FAST;
-    const int nw = f32 ? pick_warps<float>(*g, fast, red_level) : pick_warps<double>(*g, fast, red_level);
+    const int nw = f32 ? pick_warps<float>(*g, fast, red_level, t) : pick_warps<double>(*g, fast, red_level, t);
     int wps;   // resident warps per SM of that instantiation
     if (f32) wps = fast ? (red_level ? tma::Geo<float>::warps_per_sm<true, 1>() : tma::Geo<float>::warps_per_sm<true, 0>())
                         : tma::Geo<float>::warps_per_sm<false, 0>();
     else wps = tma::Geo<double>::warps_per_sm<true, 0>();
     const int own = f32 ? tma::Geo<float>::OWN : tma::Geo<double>::OWN;
-    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw);
+    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw, t);
     out[0] = nw; out[1] = p.nbands; out[2] = p.nseg; out[3] = p.sm.seg; out[4] = p.sm.tail; out[5] = p.sm.jt;
     out[6] = wps / nw;
-    return FKC_OK;
-}
-
-// test hook: warps per TMA CTA -- 0 auto, 1, 2 or 4
-int fkc_set_tma_warps(int nw) {
-    if (nw != 0 && nw != 1 && nw != 2 && nw != 4) return fail(FKC_EUSAGE, "warps per CTA must be 0 (auto), 1, 2 or 4");
-    g_warps = nw;
-    return FKC_OK;
-}
-
-// test hook: alternate the TMA kernel's sweep direction per segment (1, default) or not (0)
-int fkc_set_tma_alternate(int on) {
-    if (on != 0 && on != 1) return fail(FKC_EUSAGE, "alternate must be 0 or 1");
-    g_alt = on;
     return FKC_OK;
 }
 
@@ -507,6 +461,7 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     if (a->mode != FKC_MODE_EXACT && a->mode != FKC_MODE_FAST) return fail(FKC_EUSAGE, "invalid mode");
     if (!(a->dx > 0) || !(a->dy > 0)) return fail(FKC_EUSAGE, "dx, dy must be > 0");
     if (int rc = valid_peers(a)) return rc;
+    if (int rc = valid_tune(a->tune)) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     int variant = a->variant;
     // AUTO: the TMA sweep for grids of >= 640 Ki cells; below that (L2-
@@ -549,6 +504,7 @@ static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
             a.red.err = (uint32_t*)(out + 4);
             a.dt_bound = L->dt_from_slots ? in + 3 : nullptr;
         }
+        a.tune.parity = (int32_t)(i & 1);
         if (int rc = fkc_sw_step(&a, st)) return rc;
         if (L->slots && L->host_slots) {
             cudaError_t e = cudaMemcpyAsync(L->host_slots + 5 * (i + 1), L->slots + 5 * (i + 1), 5 * sizeof(uint64_t),

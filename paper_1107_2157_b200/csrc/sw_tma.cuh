@@ -51,8 +51,8 @@ namespace tma {
 #ifndef FKC_TMA_CTAS_F64
 #define FKC_TMA_CTAS_F64 2    // f64 kernels (~190-210 registers)
 #endif
-#ifndef FKC_TMA_CTAS_EXACT
-#define FKC_TMA_CTAS_EXACT 3  // exact kernel: <= 168 registers -> 12 warps per SM (no spills)
+#ifndef FKC_EXACT_WARPS
+#define FKC_EXACT_WARPS 12    // exact kernel: resident warps per SM (12: <= 168 registers; even)
 #endif
 constexpr int R = FKC_TMA_R;             // rows per stage
 constexpr int S = FKC_TMA_S;             // ring stages per warp
@@ -82,8 +82,8 @@ template <class T> struct Geo {
     // resident warps per SM (the FKC_TMA_CTAS_* macros count CTAs of 4 warps):
     // f32 12 (<= 168 registers), f64 8
     template <bool FAST, int RED = 0> static constexpr int warps_per_sm() {
-        return 4 * (sizeof(T) == 8 ? FKC_TMA_CTAS_F64
-                                   : (FAST ? (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_TMA_CTAS_EXACT));
+        return sizeof(T) == 8 ? 4 * FKC_TMA_CTAS_F64
+                              : (FAST ? 4 * (RED ? FKC_TMA_CTAS_FAST_RED : FKC_TMA_CTAS_FAST) : FKC_EXACT_WARPS);
     }
     static_assert(FIELD_BYTES % 128 == 0, "TMA destinations must stay 128-B aligned");
 };
@@ -104,7 +104,8 @@ template <class T, int NW> struct Blk {
 #define FKC_TMA_PAIR 1        // f32 fast mode on the packed FP32 pipe (FFMA2 / FADD2 / FMUL2)
 #endif
 #ifndef FKC_TMA_EXACT_PAIR
-#define FKC_TMA_EXACT_PAIR 1  // f32 exact mode: multiplies / division FMAs on the packed pipe
+#define FKC_TMA_EXACT_PAIR 2  // f32 exact mode: 2 = every op on the packed pipe, row-level guards
+                              // (ExactPairEngine2); 1 = packed multiplies only (ExactPairEngine); 0 = scalar
 #endif
 #ifndef FKC_FAST_UNROLL
 #define FKC_FAST_UNROLL 2     // rows of a stage unrolled in fast mode (even: the register window renames)
@@ -187,10 +188,17 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 
 // One lane's 16-byte vector of a row (4 floats or 2 doubles): shared-memory
 // load, global store.
+#ifndef FKC_LDS_PLAIN
+#define FKC_LDS_PLAIN 1   // f32: plain 128-bit shared loads (ptxas allocates the quad where the math wants it)
+#endif
 template <class T>
 __device__ __forceinline__ VecF<T> lds_vec(uint32_t a) {
     VecF<T> r;
-    if constexpr (sizeof(T) == 4)
+    if constexpr (sizeof(T) == 4 && FKC_LDS_PLAIN) {
+        float4 q;
+        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w) : "r"(a) : "memory");
+        r.v[0] = q.x; r.v[1] = q.y; r.v[2] = q.z; r.v[3] = q.w;
+    } else if constexpr (sizeof(T) == 4)
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "r"(a));
     else if constexpr (tma::Geo<T>::CPL == 2)
@@ -264,19 +272,21 @@ template <class T, int CPL>
 __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int nx, int ny, int X, int y,
                                          const BCs& bc, const Peers& P, Row3<T, CPL> o) {
     if (y == 1 || y == ny) {
-        const bool refl = (y == 1 && bc.s[SIDE_D] == BC_REFL) || (y == ny && bc.s[SIDE_U] == BC_REFL);
-        const bool per = (y == 1 && bc.s[SIDE_U] == BC_PER) || (y == ny && bc.s[SIDE_D] == BC_PER);
-        if (refl) {
-            const int64_t o2 = (int64_t)(y == 1 ? 0 : ny + 1) * pitch + X;
-            stg_vec<T, CPL>(oH + o2, o.h);
-            stg_vec<T, CPL>(oU + o2, o.u);
-            stg_vec<T, CPL>(oV + o2, o.v, T(-1));
-        }
-        if (per) {
-            const int64_t o2 = (int64_t)(y == 1 ? ny + 1 : 0) * pitch + X;
-            stg_vec<T, CPL>(oH + o2, o.h);
-            stg_vec<T, CPL>(oU + o2, o.u);
-            stg_vec<T, CPL>(oV + o2, o.v);
+        // row images of the new row: the bottom halo row (row 0) is the image
+        // of row 1 (reflective) or of row ny (periodic), the top one (row
+        // ny+1) of row ny (reflective) or row 1 (periodic) -- decided per
+        // image, so a one-row tile (y == 1 == ny) writes both
+#pragma unroll
+        for (int img = 0; img < 2; ++img) {          // 0: bottom halo row, 1: top halo row
+            const int side = img == 0 ? SIDE_D : SIDE_U;
+            const bool refl = bc.s[side] == BC_REFL && y == (img == 0 ? 1 : ny);
+            const bool per = bc.s[side] == BC_PER && y == (img == 0 ? ny : 1);
+            if (refl || per) {
+                const int64_t o2 = (int64_t)(img == 0 ? 0 : ny + 1) * pitch + X;
+                stg_vec<T, CPL>(oH + o2, o.h);
+                stg_vec<T, CPL>(oU + o2, o.u);
+                stg_vec<T, CPL>(oV + o2, o.v, refl ? T(-1) : T(1));
+            }
         }
         // fused halo exchange: the new row goes straight into the neighbour
         // tile's halo row (row lines: stride 1)
@@ -393,9 +403,10 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     // (sw_pair.cuh), scalar engine otherwise
     constexpr bool PAIR = FAST && sizeof(T) == 4 && FKC_TMA_PAIR;
     constexpr bool EXACT_PAIR = !FAST && sizeof(T) == 4 && FKC_TMA_EXACT_PAIR;
+    using ExactEngine = typename std::conditional<FKC_TMA_EXACT_PAIR == 2, ExactPairEngine2, ExactPairEngine>::type;
     using Engine = typename std::conditional<
         PAIR, PairEngine,
-        typename std::conditional<EXACT_PAIR, ExactPairEngine, ScalarEngine<T, CPL>>::type>::type;
+        typename std::conditional<EXACT_PAIR, ExactEngine, ScalarEngine<T, CPL>>::type>::type;
     Engine eng;
     eng.init(c);
     // element offset of the row updated at loaded-row index n (lane's cell 0),
@@ -404,9 +415,28 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     int64_t row_off = (int64_t)(down ? ytop + 1 : y0 - 2) * pitch + X;
     RowRed<T, FAST, RED> rr;
     rr.init();
+    T fdep = T(INFINITY);              // min face depth (fused reductions only)
     bool fix_mode = false;             // exact mode: current division variant (warp-uniform)
     int fix_rows = 0;
     constexpr int UNR = FAST ? FKC_FAST_UNROLL : (sizeof(T) == 8 ? FKC_EXACT_UNROLL_F64 : FKC_EXACT_UNROLL);
+    constexpr bool EXACT2 = EXACT_PAIR && FKC_TMA_EXACT_PAIR == 2;
+    // stores of an updated row (owner lanes): the three 16-B row vectors,
+    // then -- tile-edge lanes only, out of line to keep the sweep loop small --
+    // the output halo (boundary conditions) and the fused halo exchange, and
+    // the fused reductions
+    auto store_row = [&](int y, T (&oh)[CPL], T (&ou)[CPL], T (&ov)[CPL]) {
+        const int64_t off = row_off;
+        stg_row<T, CPL>(oH + off, oh);
+        stg_row<T, CPL>(oU + off, ou);
+        stg_row<T, CPL>(oV + off, ov);
+        if ((edge_rows && (y == 1 || y == ny)) || edge_cols) {
+            Row3<T, CPL> o;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) { o.h[i] = oh[i]; o.u[i] = ou[i]; o.v[i] = ov[i]; }
+            edge_stores<T, CPL>(oH, oU, oV, pitch, nx, ny, X, y, bc, P, o);
+        }
+        if constexpr (RED > 0) rr.template add_row<CPL>(oh, ou, ov, g);
+    };
 
     // The loop bound is re-derived from %ctaid.y (a volatile read the
     // compiler cannot hoist) instead of being kept live: in the reduction
@@ -430,27 +460,79 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                              stage_y(kn));
         }
         mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
+        // cells whose loaded data is not part of the grid become a lake at
+        // rest IN SHARED MEMORY (the lane's own 16-B slots of the stage, read
+        // back by the same lane: program order suffices; the slot's next TMA
+        // refill is ordered by the fence.proxy.async above) -- keeps the row
+        // loop free of a conditional overwrite of the loaded registers
+        if (any_bad && bad) {
+            const uint32_t s0 = ring + s * G::STAGE_BYTES + lane_off;
+#pragma unroll
+            for (int rr2 = 0; rr2 < R; ++rr2)
+#pragma unroll
+                for (int f = 0; f < 3; ++f)
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i)
+                        if (bad & (1 << i)) {
+                            const uint32_t a = s0 + rr2 * G::ROWB + f * G::FIELD_BYTES + i * (uint32_t)sizeof(T);
+                            if constexpr (sizeof(T) == 4)
+                                asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(f == 0 ? 1.0f : 0.0f) : "memory");
+                            else
+                                asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(f == 0 ? 1.0 : 0.0) : "memory");
+                        }
+        }
         // first row of the stage in sweep order (boxes are stored bottom-up)
         const uint32_t st = ring + s * G::STAGE_BYTES + lane_off + (down ? (R - 1) * G::ROWB : 0);
 #pragma unroll UNR
         for (int r = 0; r < R; ++r) {
             const int n = k * R + r;              // loaded row index; row y0-1+n (top-down: ytop-n)
             const uint32_t sr = st + r * row_bytes;
-            VecF<T> hv = lds_vec<T>(sr);
-            VecF<T> uv = lds_vec<T>(sr + G::FIELD_BYTES);
-            VecF<T> vv = lds_vec<T>(sr + 2 * G::FIELD_BYTES);
-            if (FAST) {
+            // the row's H, U, V vectors from shared memory (re-read, not kept
+            // live, when exact mode redoes the row: 12 registers fewer)
+            auto load_row = [&](VecF<T>& hv, VecF<T>& uv, VecF<T>& vv) {
+                hv = lds_vec<T>(sr);
+                uv = lds_vec<T>(sr + G::FIELD_BYTES);
+                vv = lds_vec<T>(sr + 2 * G::FIELD_BYTES);
+                if (FAST) {
 #pragma unroll
-                for (int i = 0; i < CPL; ++i) vv.v[i] *= vsign;   // mirror image (top-down sweep)
-            }
-            if (any_bad) {
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    if (bad & (1 << i)) { hv.v[i] = T(1); uv.v[i] = T(0); vv.v[i] = T(0); }
-            }
+                    for (int i = 0; i < CPL; ++i) vv.v[i] *= vsign;   // mirror image (top-down sweep)
+                }
+            };
+            VecF<T> hv, uv, vv;
+            load_row(hv, uv, vv);
             const bool have_prev = n >= 1;
             const bool want_x = (n >= 1) && (n <= nrows);
+            const bool upd = (n >= 2) && (n <= nrows + 1);
+            const int y_upd = down ? ytop - n + 1 : y0 + n - 2;   // row updated at this step
             bool ok = true;
+            if constexpr (EXACT2) {
+                // exact mode, two guarded phases per row (sw_pair.cuh
+                // ExactPairEngine2); a phase that saw a non-benign operand or a
+                // subnormal tie in any lane is redone with DIV_FIXUP
+                eng.template cells_y<DIV_GUARD>(hv, uv, vv, have_prev, ok);
+                if (__any_sync(0xffffffffu, !ok)) {
+                    VecF<T> h2, u2, v2;
+                    asm volatile("" ::: "memory");       // a fresh shared load, not the first one kept live
+                    load_row(h2, u2, v2);
+                    eng.template cells_y<DIV_FIXUP>(h2, u2, v2, have_prev, ok);
+                }
+                if (upd) {
+                    T oh[CPL], ou[CPL], ov[CPL];
+                    eng.template update<DM>(c, oh, ou, ov);
+                    if (owner) store_row(y_upd, oh, ou, ov);
+                }
+                bool okx = true;
+                eng.template xfaces<DIV_GUARD>(want_x, okx);
+                if (__any_sync(0xffffffffu, !okx)) eng.template xfaces<DIV_FIXUP>(want_x, okx);
+                if constexpr (RED > 0) {
+                    const bool xrow = (n >= 1) && (n <= nrows);
+                    const bool yrow = (n >= 1) && (n <= nrows + 1);
+                    eng.track(fdep, owner && xrow, lane == 0 && xrow, owner && yrow);
+                }
+                row_off += row_step;
+                eng.shift();
+                continue;
+            }
             if constexpr (FAST) {
                 // branch-free: the faces of the first loaded row / of rows past the
                 // segment are computed on benign or discarded data, never stored
@@ -468,38 +550,34 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                     if (__any_sync(0xffffffffu, !ok)) {
                         fix_mode = FKC_FIX_PERSIST > 0;
                         fix_rows = 0;
-                        eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
+                        VecF<T> h2, u2, v2;
+                        asm volatile("" ::: "memory");   // a fresh shared load, not the first one kept live
+                        load_row(h2, u2, v2);
+                        eng.template row<DIV_FIXUP>(h2, u2, v2, have_prev, want_x, c, ok);
                     }
                 } else {
                     eng.template row<DIV_FIXUP>(hv, uv, vv, have_prev, want_x, c, ok);
                     if (++fix_rows >= FKC_FIX_PERSIST) fix_mode = false;
                 }
             }
+            if constexpr (RED > 0) {
+                // face depths of the faces owned cells use (NonPositiveDepth:
+                // any face or cell h <= 0): x-faces of the
+                // segment's rows, y-faces from below its first row to above
+                // its last
+                const bool xrow = (n >= 1) && (n <= nrows);
+                const bool yrow = (n >= 1) && (n <= nrows + 1);
+                eng.track(fdep, owner && xrow, lane == 0 && xrow, owner && yrow);
+            }
             // full-step update of the previous row (row y0 + n - 2; top-down: ytop - n + 1)
-            const bool upd = (n >= 2) && (n <= nrows + 1);
             if (FAST || upd) {
-                const int y = down ? ytop - n + 1 : y0 + n - 2;
                 T oh[CPL], ou[CPL], ov[CPL];
                 eng.template update<DM>(c, oh, ou, ov);
                 if (FAST) {
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) ov[i] *= vsign;   // back from the mirror image
                 }
-                const int64_t off = row_off;
-                if (owner && upd) {
-                    stg_row<T, CPL>(oH + off, oh);
-                    stg_row<T, CPL>(oU + off, ou);
-                    stg_row<T, CPL>(oV + off, ov);
-                    // output halo (boundary conditions) and fused halo exchange:
-                    // tile-edge lanes only, out of line to keep the sweep loop small
-                    if ((edge_rows && (y == 1 || y == ny)) || edge_cols) {
-                        Row3<T, CPL> o;
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) { o.h[i] = oh[i]; o.u[i] = ou[i]; o.v[i] = ov[i]; }
-                        edge_stores<T, CPL>(oH, oU, oV, pitch, nx, ny, X, y, bc, P, o);
-                    }
-                    if constexpr (RED > 0) rr.template add_row<CPL>(oh, ou, ov, g);
-                }
+                if (owner && upd) store_row(y_upd, oh, ou, ov);
             }
             row_off += row_step;
             // shift the register window (renamed away by the unrolled loop)
@@ -514,7 +592,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         const int expected[4] = {(int)gridDim.y, (int)gridDim.y, nstrips, nstrips};
         if (lane == 0) peer_signal(sy, sides, expected);
     }
-    if constexpr (RED > 0) rr.commit(red, lane, dmin);
+    if constexpr (RED > 0) rr.commit(red, lane, dmin, fdep);
 }
 
 }  // namespace fkc

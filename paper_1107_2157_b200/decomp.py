@@ -25,7 +25,6 @@ validate the GPU path on a single device).
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -539,6 +538,7 @@ class DistributedSimulation:
                 bound = self.slots.addr(self.n, 3) if self.cfl else None
                 a = swdemo._step_args(src, dst, cfg.dt if cfg.dt is not None else 0.0, self.bc, cfg.mode,
                                       cfg.variant, red, bound, cfg.cfl_factor)
+                a.tune.parity = self.n & 1          # alternating segment order (L2 reuse)
                 if self.transport == "peer":
                     out_parity = (self.n + 1) % 2
                     for s, line in self.peer.lines[out_parity].items():
@@ -692,6 +692,7 @@ def run_local_decomposed(cfg, px: int, py: int, steps: int, device=None, exchang
         for r in range(grid.size):
             src, dst = bufs[r][k % 2], bufs[r][(k + 1) % 2]
             a = swdemo._step_args(src, dst, cfg.dt, grid.local_bc(r), cfg.mode, cfg.variant)
+            a.tune.parity = k & 1
             for s, line in lines[r][(k + 1) % 2].items():
                 a.peer[s] = line
             if concurrent:
@@ -718,142 +719,3 @@ def gather_interior(grid: CartGrid, tiles: Sequence[np.ndarray]) -> np.ndarray:
         t = grid.tile(r)
         out[t.y0:t.y0 + t.ny, t.x0:t.x0 + t.nx] = a
     return out
-
-
-# ---------------------------------------------------------------------------
-# bench entry (torchrun, N > 1): weak scaling, 16384^2 cells per GPU
-# ---------------------------------------------------------------------------
-
-def bench_main(args, rank: int, world: int) -> int:
-    import json
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    from . import swdemo
-
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    # FKC_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo host collectives
-    # -- exercises the N>1 code path (IPC peer memory, mailboxes) on a
-    # one-GPU box; its timings are meaningless (time-sliced contexts)
-    one_dev = os.environ.get("FKC_BENCH_ONE_DEVICE") == "1"
-    if one_dev:
-        local = 0
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if one_dev:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=dev)
-    px, py = choose_grid(world)
-    n = args.n
-    strong = bool(getattr(args, "global_n", 0))
-    # weak scaling (default): n^2 cells per GPU; strong: a fixed global grid
-    grid = CartGrid(px, py, args.global_n, args.global_n, "reflective") if strong else \
-        CartGrid(px, py, px * n, py * n, "reflective")
-    # fixed dt = 0.3 * stable_dt of the initial global state (h max 1.4, u = v = 0)
-    dt = 0.3 * 1.0 / float(np.sqrt(np.float32(9.8) * np.float32(1.4)))
-    cfg = swdemo.SWConfig(nx=grid.NX, ny=grid.NY, dt=dt, mode=args.mode, variant=args.variant)
-    from bench import ClockSampler
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.stream(stream):
-        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport)
-        sim.advance(args.warmup)
-        torch.cuda.synchronize()
-        dist.barrier()
-        clocks = ClockSampler(local) if rank == 0 else None
-        if clocks:
-            clocks.__enter__()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        sim.advance(args.steps)
-        t1.record(stream)
-        torch.cuda.synchronize()
-        if clocks:
-            clocks.__exit__(None, None, None)
-        dist.barrier()
-    ms = torch.tensor([t0.elapsed_time(t1)], device="cpu" if one_dev else dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    total_ms = float(ms.item())
-    launches = sim._launches_per_step()
-    transport, fallback = sim.transport, sim.fallback_reason
-    sim.close()
-    del sim
-    torch.cuda.empty_cache()
-    e2e = None if getattr(args, "no_e2e", False) else _bench_e2e(args, cfg, grid, rank, world, dev, one_dev)
-    cells = grid.NX * grid.NY
-    value = cells * args.steps / (total_ms / 1e3) / 1e9
-    if rank == 0:
-        from bench import BYTES_PER_CELL, peaks
-        peak, src = peaks()
-        per_gpu_gbs = BYTES_PER_CELL["f32"] * (cells / world) * args.steps / (total_ms / 1e3) / 1e9
-        from bench import METRIC, workload
-        line = {"metric": METRIC, "value": round(value, 3),
-                "unit": "Gcell-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
-                "scaling": "strong" if strong else "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Gaussian hump)",
-                "config": {"workload": (f"shallow-water {grid.NX}x{grid.NY} fp32 2-D decomposed {px}x{py}, "
-                                        "reflective, fixed dt=0.3*stable_dt (BASELINE config 4, strong scaling)")
-                           if strong else workload(n, world),
-                           "exchange": "one-cell halo exchange per step " +
-                                       ("fused into the step kernel (NVLink peer stores + mailbox flags)"
-                                        if transport == "peer" else "(pack + NCCL send/recv + unpack)"),
-
-                           "global": f"{grid.NX}x{grid.NY}", "mode": args.mode, "parallelism": f"domain{px}x{py}"},
-                "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1), "peak": peak, "unit": "GB/s",
-                             "frac": round(per_gpu_gbs / peak, 4), "peak_source": src,
-                             "note": "per-GPU HBM rate of the whole step incl. exchange", "traffic": None},
-                "gpu_launches": args.steps * launches,
-                "clocks": clocks.summary()}
-        if e2e is not None:
-            line["e2e"] = e2e
-        line["config"]["transport"] = transport
-        if fallback:
-            line["config"]["transport_fallback"] = fallback[:300]
-        print(json.dumps(line))
-    dist.destroy_process_group()
-    return 0
-
-
-def _bench_e2e(args, cfg, grid: CartGrid, rank: int, world: int, dev, one_dev: bool):
-    """End to end through the public API at N GPUs: every rank's tile
-    starts in pinned host memory, DistributedSimulation uploads it, sets up
-    the exchange, advances `steps` steps and the final tile is copied back;
-    wall clock between two barriers, max over ranks."""
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    from . import swdemo
-    from .field import Field
-    t = grid.tile(rank)
-    full = Extent(t.nx + 2, t.ny + 2)
-    steps = max(args.steps, 200)
-    pin = [torch.zeros((t.ny + 2, t.nx + 2), dtype=torch.float32, pin_memory=True) for _ in range(6)]
-    pin[0][1:-1, 1:-1] = torch.from_numpy(gaussian_tile(grid, rank, "f32", cfg.dx, cfg.dy, cfg.base,
-                                                        cfg.amplitude, cfg.center, cfg.width))
-    host_in = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[:3]), cfg.g, cfg.dx, cfg.dy)
-    host_out = swdemo.SWState(*(Field(full, p.numpy(), "f32") for p in pin[3:]), cfg.g, cfg.dx, cfg.dy)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t0 = time.perf_counter()
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.stream(stream):
-        sim = DistributedSimulation(cfg, grid, rank, dev, stream=stream, transport=args.transport, state=host_in)
-        sim.advance(steps)
-        sim.state().to_host(host_out)
-    torch.cuda.synchronize()
-    el = time.perf_counter() - t0
-    sim.close()
-    dist.barrier()
-    tt = torch.tensor([el], dtype=torch.float64, device="cpu" if one_dev else dev)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    el = float(tt.item())
-    state_bytes = 3 * 4 * (t.nx + 2) * (t.ny + 2) * world
-    return {"value": round(grid.NX * grid.NY * steps / el / 1e9, 3), "unit": "Gcell-updates/s",
-            "h2d_bytes_per_step": round(state_bytes / steps, 1), "d2h_bytes_per_step": round(state_bytes / steps, 1),
-            "steps": steps, "api": "DistributedSimulation(cfg, grid, rank, state=<host pinned tile>) -> "
-                                   "advance(steps) -> state().to_host(<host pinned tile>)"}

@@ -201,5 +201,5 @@ class DeviceField:
         return self.to_numpy().tobytes()
 
     def __repr__(self):
-        return (f"DeviceField(full={tuple(self.full)}, precision={self.precision!r}, "
+        return (f"DeviceField(full=({self.full.nx}, {self.full.ny}), precision={self.precision!r}, "
                 f"pitch={self.pitch}, device={self.storage.device})")

@@ -44,8 +44,16 @@ class NonfiniteValue(ArithmeticError):
     """NaN/Inf in the state."""
 
 
-class LaunchError(ValueError):
-    """Invalid launch configuration."""
+class LaunchError(N.FkcUsageError):
+    """Invalid launch configuration: raised for every
+    usage error the C-ABI reports (FKC_EUSAGE -- bad extent, pitch,
+    alignment, enum, aliasing), before any device memory is touched.  A
+    ``ValueError``, like the reference's."""
+
+    def __init__(self, code_or_msg, msg=None):
+        if msg is None:
+            code_or_msg, msg = N.FKC_EUSAGE, str(code_or_msg)
+        super().__init__(code_or_msg, msg)
 
 
 @dataclass
@@ -122,8 +130,11 @@ class SWState:
         return SWState(*(DeviceField.from_field(f, device) for f in (self.H, self.U, self.V)),
                        self.g, self.dx, self.dy, self.t)
 
-    def to_host(self, out: Optional["SWState"] = None) -> "SWState":
-        """Device -> host Fields (into `out`'s arrays when given, e.g. pinned)."""
+    def to_host(self, out: Optional["SWState"] = None, like: Optional["SWState"] = None) -> "SWState":
+        """Device -> host Fields (into `out`'s arrays when given, e.g. pinned).
+        With ``like`` (a host state), the new Fields are of ``like``'s Field
+        class -- e.g. the reference's own ``fkc.field.Field`` -- so a caller
+        of the reference API gets its own types back."""
         if not self.on_device:
             return self
         if out is not None:
@@ -131,6 +142,10 @@ class SWState:
                 getattr(self, name).to_field(getattr(out, name))
             out.g, out.dx, out.dy, out.t = self.g, self.dx, self.dy, self.t
             return out
+        if like is not None and not isinstance(like.H, Field):
+            mk = lambda dev, tmpl: type(tmpl)(tmpl.full, dev.to_numpy(), dev.precision)  # noqa: E731
+            return SWState(mk(self.H, like.H), mk(self.U, like.U), mk(self.V, like.V),
+                           self.g, self.dx, self.dy, self.t)
         return SWState(self.H.to_field(), self.U.to_field(), self.V.to_field(),
                        self.g, self.dx, self.dy, self.t)
 
@@ -207,6 +222,8 @@ def raise_for_error(err_word: int, where: str = ""):
         raise RuntimeError(f"device watchdog fired {where}")
     if err_word & N.ERR_NONFINITE:
         raise NonfiniteValue(f"non-finite state {where}")
+    if err_word & N.ERR_NONPOSITIVE_FACE:
+        raise NonPositiveDepth(f"face depth <= 0 {where}")
     if err_word & N.ERR_NONPOSITIVE_DEPTH:
         raise NonPositiveDepth(f"depth <= 0 {where}")
 
@@ -279,7 +296,8 @@ def total_mass(state: SWState) -> float:
 
 
 def _step_args(src: SWState, dst: SWState, dt: float, boundary, mode: str, variant: str,
-               red: Optional[N.Reduce] = None, dt_bound: Optional[int] = None, cfl: float = 1.0) -> N.StepArgs:
+               red: Optional[N.Reduce] = None, dt_bound: Optional[int] = None, cfl: float = 1.0,
+               tune: Optional[N.Tune] = None) -> N.StepArgs:
     a = N.StepArgs()
     a.grid = _grid(src.H)
     a.H, a.U, a.V = src.H.ptr, src.U.ptr, src.V.ptr
@@ -292,29 +310,52 @@ def _step_args(src: SWState, dst: SWState, dt: float, boundary, mode: str, varia
     a.variant = VARIANTS[variant]
     if red is not None:
         a.red = red
+    if tune is not None:
+        a.tune = tune
     return a
 
 
 def advance(state: SWState, dt: float, boundary="reflective", mode: str = "exact",
-            variant: str = "auto", out: Optional[SWState] = None, stream=None) -> SWState:
+            variant: str = "auto", out: Optional[SWState] = None, stream=None,
+            tune: Optional[N.Tune] = None, check: bool = False) -> SWState:
     """Engine contract ``advance(state, dt) -> state``: one
     Lax-Wendroff step into fresh (or given) buffers; the input state is never
     mutated.  The output halo is filled per ``boundary``
-    in the same kernel (== apply_boundary of the new state)."""
+    in the same kernel (== apply_boundary of the new state).
+
+    ``check=True`` adds step_native's domain check: the input
+    depths are reduced on device and the step kernel reports its half-step
+    face depths; :class:`NonPositiveDepth` is raised if any face or input
+    cell depth is <= 0 (one synchronisation).  ``tune`` is the per-call
+    launch schedule (``_native.Tune``; results never depend on it)."""
     host = not state.on_device
     src = _as_device(state)
     if out is None:
         out = SWState(src.H.empty_like(), src.U.empty_like(), src.V.empty_like(), src.g, src.dx, src.dy, src.t)
-    a = _step_args(src, out, dt, boundary, mode, variant)
+    slots = None
+    red = None
+    if check:
+        slots = ReductionSlots(2, src.H.storage.device)
+        g = _grid(src.H)
+        red0 = slots.reduce_struct(0, mass=False, maxima=False, cfl=False)
+        N.check(N.lib().fkc_sw_reduce_state(ctypes.byref(g), src.H.ptr, src.U.ptr, src.V.ptr, src.dx, src.dy,
+                                            src.g, ctypes.byref(red0), _stream_ptr(stream)))
+        red = slots.reduce_struct(1, mass=False, maxima=False, cfl=False)
+    a = _step_args(src, out, dt, boundary, mode, variant, red=red, tune=tune)
     N.check(N.lib().fkc_sw_step(ctypes.byref(a), _stream_ptr(stream)))
+    if slots is not None:
+        err = ReductionSlots.decode(slots.buf.cpu().numpy())["err"]
+        if (err[0] & N.ERR_NONPOSITIVE_DEPTH) or (err[1] & N.ERR_NONPOSITIVE_FACE):
+            raise NonPositiveDepth("face or cell depth <= 0")
     out.t = src.t + float(dt)
-    return out.to_host() if host else out
+    return out.to_host(like=state) if host else out
 
 
 def step_native(state: SWState, dt: float, boundary="reflective", mode: str = "exact") -> SWState:
     """Name-compatible alias of the reference's ``step_native``
-    -- executed by the CUDA kernel."""
-    return advance(state, dt, boundary, mode)
+    -- executed by the CUDA kernel, with its NonPositiveDepth check
+    (SPEC.md:524)."""
+    return advance(state, dt, boundary, mode, check=True)
 
 
 # ---------------------------------------------------------------------------
@@ -339,13 +380,16 @@ class Simulation:
     """
 
     def __init__(self, cfg: SWConfig, state: Optional[SWState] = None, diagnostics: bool = True,
-                 capacity: Optional[int] = None, stream=None, boundary=None, stream_rows: bool = False):
+                 capacity: Optional[int] = None, stream=None, boundary=None, stream_rows: bool = False,
+                 tune: Optional[N.Tune] = None):
         torch = _torch()
         self.cfg = cfg
+        self.tune = tune
         self.stream = stream
         self.boundary = boundary if boundary is not None else cfg.boundary
         st = state if state is not None else init_state(cfg)
         st = _as_device(st)
+        self.t0 = st.t          # a resumed state keeps its clock (rows() continues from it)
         self.a = st
         self.b = SWState(st.H.empty_like(), st.U.empty_like(), st.V.empty_like(), st.g, st.dx, st.dy, st.t)
         self.diag = diagnostics or cfg.dt is None
@@ -373,7 +417,7 @@ class Simulation:
         cfg = self.cfg
         L = N.LoopArgs()
         L.step = _step_args(self.a, self.b, cfg.dt if cfg.dt is not None else 0.0, self.boundary, cfg.mode,
-                            cfg.variant, None, None, cfg.cfl_factor)
+                            cfg.variant, None, None, cfg.cfl_factor, self.tune)
         L.first_step = first
         L.steps = steps
         if self.diag:
@@ -442,7 +486,10 @@ class Simulation:
         f = dtype_of(cfg.precision).type
         rows = []
         dts = []
-        t = 0.0
+        t = self.t0
+        # the steps run with the state's own spacing (SWState.dx / dy), so the
+        # mass does too
+        cell_area = self.a.dx * self.a.dy
         if d["err"][0]:
             raise_for_error(int(d["err"][0]), "in the initial state")
         for k in range(self.n):
@@ -451,7 +498,7 @@ class Simulation:
             dt = float(cfg.dt) if cfg.dt is not None else float(f(cfg.cfl_factor) * f(d["cfl_min"][k]))
             t += dt
             dts.append(dt)
-            rows.append((k + 1, t, dt, float(d["mass"][k + 1]) * cfg.dx * cfg.dy,
+            rows.append((k + 1, t, dt, float(d["mass"][k + 1]) * cell_area,
                          float(d["max_hu"][k + 1]), float(d["max_hv"][k + 1])))
         st = self.state()
         st.t = t

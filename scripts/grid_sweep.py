@@ -26,9 +26,9 @@ def main():
     ap.add_argument("--segs", default="0", help="comma list of TMA segment lengths to try (0 = auto)")
     ap.add_argument("--variants", default="auto", help="comma list of kernel variants (auto, tma, generic)")
     ap.add_argument("--warps", default="0", help="comma list of warps per TMA CTA (0 auto, 1, 2, 4)")
-    ap.add_argument("--orders", default="2", help="comma list of TMA segment orders (0 bottom-up, 2 alternating)")
+    ap.add_argument("--orders", default="0", help="comma list of TMA segment orders (fkc_sw_tune.order: 0 alternating, 1 bottom-up)")
     ap.add_argument("--pdl", default="1", help="comma list: programmatic dependent launch on (1) / off (0)")
-    ap.add_argument("--tails", default="-1:1", help="comma list of guided-segmentation settings rows:waves (-1 auto, 0 off)")
+    ap.add_argument("--tails", default="0:1", help="comma list of guided-segmentation settings rows:waves (fkc_sw_tune: 0 auto, -1 off)")
     args = ap.parse_args()
     import torch
 
@@ -43,19 +43,16 @@ def main():
             for v in args.variants.split(",") for t in args.tails.split(",") for p in args.pdl.split(",")
             for o in args.orders.split(",") for w in args.warps.split(",")]
     for n, seg, variant, tail, pdl, order, warps in todo:
-        N.check(N.lib().fkc_set_tma_warps(int(warps)))
-        N.check(N.lib().fkc_set_pdl(pdl))
-        N.check(N.lib().fkc_set_tma_order(order))
         if variant == "generic" and seg:
             continue
-        N.check(N.lib().fkc_set_tma_segment(seg))
-        N.check(N.lib().fkc_set_tma_tail(*(int(x) for x in tail.split(":"))))
+        tr, tw = (int(x) for x in tail.split(":"))
+        tune = N.Tune(warps=int(warps), no_pdl=1 - pdl, order=order, seg=seg, tail_rows=tr, tail_waves=tw)
         st = device_gaussian_state(n, n, dev)
         dt = 0.3 * swdemo.stable_dt(st, 1.0)
         cfg = swdemo.SWConfig(nx=n, ny=n, dt=dt, mode=args.mode, variant=variant)
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
-            sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+            sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream, tune=tune)
             k = 20 if n >= 4096 else 200
             replay = sim.capture(k)
             for _ in range(2):

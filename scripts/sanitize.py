@@ -25,20 +25,20 @@ def main():
 
     torch.cuda.set_device(0)
     # optional overrides (isolating a sanitizer report): FKC_SAN_PDL=0|1, FKC_SAN_WARPS=0|1|2|4
-    if os.environ.get("FKC_SAN_PDL"):
-        N.check(N.lib().fkc_set_pdl(int(os.environ["FKC_SAN_PDL"])))
-    if os.environ.get("FKC_SAN_WARPS"):
-        N.check(N.lib().fkc_set_tma_warps(int(os.environ["FKC_SAN_WARPS"])))
+    base = N.Tune(no_pdl=1 - int(os.environ.get("FKC_SAN_PDL", "1")), warps=int(os.environ.get("FKC_SAN_WARPS", "0")))
     for prec in ("f32", "f64"):
         H, U, V = so.random_state(488, 70, prec, seed=3)
         st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, prec)) for a in (H, U, V)))
         for mode in ("exact", "fast"):
             for variant in ("tma", "generic"):
                 for alt in (0, 1):
-                    N.check(N.lib().fkc_set_tma_alternate(alt))
-                    N.check(N.lib().fkc_set_tma_segment(16))
-                    out = swdemo.advance(st, 0.05, "reflective", mode, variant)
-                    swdemo.advance(out, 0.05, "periodic", mode, variant)
+                    t = base.copy()
+                    t.no_alternate, t.seg = 1 - alt, 16
+                    out = swdemo.advance(st, 0.05, "reflective", mode, variant, tune=t)
+                    t2 = t.copy()
+                    t2.parity = 1
+                    swdemo.advance(out, 0.05, "periodic", mode, variant, tune=t2)
+                    swdemo.advance(out, 0.05, "reflective", mode, variant, tune=t2, check=True)
         for mode in ("exact", "fast"):
             cfg = swdemo.SWConfig(nx=488, ny=70, steps=3, cfl_factor=0.5, precision=prec, mode=mode)
             swdemo.run(cfg)
@@ -48,17 +48,17 @@ def main():
         swdemo.apply_boundary(st, "periodic")
         refinterp.region_cpy(st.H, (1, 0, 1, 1))
         refinterp.cshift(st.U, 1, 3)
-    N.check(N.lib().fkc_set_tma_segment(0))
-    N.check(N.lib().fkc_set_tma_alternate(1))
     # guided segmentation (short tail segments) on a tall grid, chained steps
     # (programmatic dependent launch between them)
     H, U, V = so.random_state(128, 4000, "f32", seed=4)
     st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, "f32")) for a in (H, U, V)))
-    N.check(N.lib().fkc_set_tma_tail(2, 1))
+    t = base.copy()
+    t.tail_rows = 2
     for mode in ("exact", "fast"):
-        out = swdemo.advance(st, 0.05, "reflective", mode, "tma")
-        swdemo.advance(out, 0.05, "reflective", mode, "tma")
-    N.check(N.lib().fkc_set_tma_tail(-1, 1))
+        out = swdemo.advance(st, 0.05, "reflective", mode, "tma", tune=t)
+        t1 = t.copy()
+        t1.parity = 1
+        swdemo.advance(out, 0.05, "reflective", mode, "tma", tune=t1)
     for ex, conc in (("pack", False), ("fused", False), ("fused", True)):
         cfg = swdemo.SWConfig(nx=480, ny=256, dt=0.05, boundary="periodic", mode="fast")
         run_local_decomposed(cfg, 2, 2, 3, exchange=ex, concurrent=conc)

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(N.EXPORTS), (names, N.EXPORTS)
     for name in names:
         assert hasattr(L, name), name
-    assert L.fkc_abi_version() == N.ABI_VERSION == 2
+    assert L.fkc_abi_version() == N.ABI_VERSION == 3
 
 
 def test_usage_errors_without_gpu():
@@ -43,10 +43,16 @@ def test_usage_errors_without_gpu():
     assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE   # aliasing
     halo = (ctypes.c_int32 * 4)(3, 3, 0, 0)
     assert L.fkc_region_cpy(0, 16, 5, 5, 5, halo, 32, 5, None) == N.FKC_EDOMAIN  # HaloTooLarge
-    assert L.fkc_set_tma_segment(-1) == N.FKC_EUSAGE
-    assert L.fkc_set_pdl(2) == N.FKC_EUSAGE and L.fkc_set_tma_order(3) == N.FKC_EUSAGE
-    assert L.fkc_set_tma_warps(3) == N.FKC_EUSAGE
-    assert L.fkc_set_tma_tail(-2, 1) == N.FKC_EUSAGE and L.fkc_set_tma_tail(4, 0) == N.FKC_EUSAGE
+    # per-call schedule (fkc_sw_tune): invalid values are usage errors before any device work
+    a.grid = N.Grid(8, 8, 12, 0, 0)
+    a.H, a.U, a.V, a.oH, a.oU, a.oV = 1024, 2048, 3072, 4096, 5120, 6144
+    a.dx = a.dy = 1.0
+    for bad in (dict(seg=-1), dict(tail_rows=-2), dict(tail_waves=65), dict(order=3), dict(parity=2),
+                dict(warps=3), dict(no_pdl=2), dict(no_alternate=-1)):
+        a.tune = N.Tune(**bad)
+        assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE, bad
+        assert b"tune" in L.fkc_last_error()
+    a.tune = N.Tune()
     # fused exchange: a peer line needs bc NONE on its side, and wait/signal come in pairs
     a.grid = N.Grid(8, 8, 12, 0, 0)
     a.H, a.U, a.V, a.oH, a.oU, a.oV = 1024, 2048, 3072, 4096, 5120, 6144
@@ -94,6 +100,8 @@ def test_struct_layout_matches_header():
       printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_peer_line), sizeof(fkc_sync),
              offsetof(fkc_sw_step_args, peer), offsetof(fkc_sw_step_args, sync),
              offsetof(fkc_sync, counter), offsetof(fkc_sync, epoch));
+      printf("%zu %zu %zu %zu\n", sizeof(fkc_sw_tune), offsetof(fkc_sw_step_args, tune),
+             offsetof(fkc_sw_tune, parity), offsetof(fkc_sw_tune, no_alternate));
       printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fkc_sw_loop_args), offsetof(fkc_sw_loop_args, first_step),
              offsetof(fkc_sw_loop_args, slots), offsetof(fkc_sw_loop_args, want_cfl),
              offsetof(fkc_sw_loop_args, use_graph), offsetof(fkc_sw_loop_args, host_slots));
@@ -112,6 +120,7 @@ def test_struct_layout_matches_header():
             S.H.offset, S.dx.offset, S.dt_bound.offset, S.bc.offset, S.variant.offset, S.red.offset,
             ctypes.sizeof(N.PeerLine), ctypes.sizeof(N.Sync), S.peer.offset, S.sync.offset,
             N.Sync.counter.offset, N.Sync.epoch.offset,
+            ctypes.sizeof(N.Tune), S.tune.offset, N.Tune.parity.offset, N.Tune.no_alternate.offset,
             ctypes.sizeof(N.LoopArgs), N.LoopArgs.first_step.offset, N.LoopArgs.slots.offset,
             N.LoopArgs.want_cfl.offset, N.LoopArgs.use_graph.offset, N.LoopArgs.host_slots.offset]
     assert got == want

@@ -14,10 +14,11 @@ from paper_1107_2157_b200 import _native as N
 SM = 148   # no device here: the library falls back to the B200's SM count
 
 
-def plan(n, mode="fast", red=0, prec="f32", ny=None):
+def plan(n, mode="fast", red=0, prec="f32", ny=None, tune=None):
     g = N.Grid(n, ny or n, n + 32, N.F32 if prec == "f32" else N.F64, 0)
     out = (ctypes.c_int * 7)()
-    N.check(N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if mode == "fast" else N.MODE_EXACT, red, out))
+    N.check(N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST if mode == "fast" else N.MODE_EXACT, red,
+                                 ctypes.byref(tune) if tune is not None else None, out))
     keys = ("warps", "bands", "nseg", "seg", "tail", "jt", "ctas_per_sm")
     return dict(zip(keys, list(out)))
 
@@ -56,7 +57,20 @@ def test_plan_choices():
 def test_plan_usage_errors():
     g = N.Grid(0, 16, 32, N.F32, 0)
     out = (ctypes.c_int * 7)()
-    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 0, out) == N.FKC_EUSAGE
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 0, None, out) == N.FKC_EUSAGE
     g = N.Grid(64, 16, 96, N.F32, 0)
-    assert N.lib().fkc_tma_plan(ctypes.byref(g), 7, 0, out) == N.FKC_EUSAGE
-    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 3, out) == N.FKC_EUSAGE
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), 7, 0, None, out) == N.FKC_EUSAGE
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 3, None, out) == N.FKC_EUSAGE
+    bad = N.Tune(warps=3)
+    assert N.lib().fkc_tma_plan(ctypes.byref(g), N.MODE_FAST, 0, ctypes.byref(bad), out) == N.FKC_EUSAGE
+
+
+def test_plan_tune_is_per_call():
+    """The schedule knobs travel in the argument block (fkc_sw_tune), so one
+    caller's forced schedule never leaks into another's (ABI 3)."""
+    forced = plan(16384, tune=N.Tune(seg=14, warps=2))
+    assert forced["seg"] == 14 and forced["warps"] == 2 and forced["tail"] == 0
+    assert plan(16384) == plan(16384, tune=N.Tune())
+    assert plan(16384)["seg"] == 30 and plan(16384)["warps"] == 4
+    tail = plan(16384, tune=N.Tune(tail_rows=-1))
+    assert tail["tail"] == 0 and tail["seg"] == 30
