@@ -113,6 +113,9 @@ template <class T, int NW> struct Blk {
 #ifndef FKC_FIX_PERSIST
 #define FKC_FIX_PERSIST 0     // exact mode: rows that stay on the fixup variant after a guard failure
 #endif
+#ifndef FKC_EXACT_ROWSYNC
+#define FKC_EXACT_ROWSYNC 0
+#endif
 #ifndef FKC_EXACT_UNROLL
 #define FKC_EXACT_UNROLL 1    // exact f32 rows unrolled (1: the loop body stays in the I-cache)
 #endif
@@ -531,6 +534,9 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
                 }
                 row_off += row_step;
                 eng.shift();
+#if FKC_EXACT_ROWSYNC
+                __syncwarp();      // keeps ptxas from interleaving unrolled rows (register peak)
+#endif
                 continue;
             }
             if constexpr (FAST) {

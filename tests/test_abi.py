@@ -158,3 +158,93 @@ def test_integration_c_example_compiles_and_links():
         r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "null" in r.stderr
+
+
+C_MAIN = r"""
+#include <stdlib.h>
+#include <string.h>
+#include <cuda_runtime.h>
+
+/* reads nx ny K and the initial H,U,V ((ny+2) x (nx+2) f32 each) from argv[1];
+ * writes the state after one_step (fast) and after many_steps (exact, K steps)
+ * to argv[2] */
+int main(int argc, char** argv) {
+    FILE* f = fopen(argv[1], "rb");
+    int hdr[3];
+    if (!f || fread(hdr, 4, 3, f) != 3) return 10;
+    const int nx = hdr[0], ny = hdr[1], K = hdr[2];
+    const long W = nx + 2, Hh = ny + 2, pitch = (W + 31) / 32 * 32;
+    const size_t n_host = (size_t)W * Hh;
+    float* host = (float*)malloc(3 * n_host * 4);
+    if (fread(host, 4, 3 * n_host, f) != 3 * n_host) return 11;
+    fclose(f);
+    void* base[6];
+    float* ptr[6];
+    for (int i = 0; i < 6; ++i) {
+        /* the layout DeviceField uses: (ptr + 1 element) 128-B aligned, 31 readable floats before ptr */
+        if (cudaMalloc(&base[i], (31 + Hh * pitch + 32) * 4) != cudaSuccess) return 12;
+        ptr[i] = (float*)base[i] + 31;
+    }
+    for (int i = 0; i < 3; ++i)
+        cudaMemcpy2D(ptr[i], pitch * 4, host + i * n_host, W * 4, W * 4, Hh, cudaMemcpyHostToDevice);
+    FILE* o = fopen(argv[2], "wb");
+    if (one_step(nx, ny, pitch, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], ptr[5], 0.05, 0) != FKC_OK) return 13;
+    cudaDeviceSynchronize();
+    for (int i = 3; i < 6; ++i) {
+        cudaMemcpy2D(host, W * 4, ptr[i], pitch * 4, W * 4, Hh, cudaMemcpyDeviceToHost);
+        fwrite(host, 4, n_host, o);
+    }
+    fkc_sw_step_args t = {0};
+    t.grid = (fkc_grid){nx, ny, pitch, FKC_F32, 0};
+    t.H = ptr[0]; t.U = ptr[1]; t.V = ptr[2]; t.oH = ptr[3]; t.oU = ptr[4]; t.oV = ptr[5];
+    t.dx = t.dy = 1.0; t.dt = 0.05; t.g = 9.8;
+    t.mode = FKC_MODE_EXACT;
+    if (many_steps(&t, K, 0) != FKC_OK) { fprintf(stderr, "%s\n", fkc_last_error()); return 14; }
+    if (cudaDeviceSynchronize() != cudaSuccess) return 15;
+    for (int i = 0; i < 3; ++i) {
+        cudaMemcpy2D(host, W * 4, ptr[(K % 2) ? 3 + i : i], pitch * 4, W * 4, Hh, cudaMemcpyDeviceToHost);
+        fwrite(host, 4, n_host, o);
+    }
+    fclose(o);
+    return 0;
+}
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nx,ny,K", [(1024, 700, 5), (516, 130, 4)])
+def test_integration_c_example_on_device(nx, ny, K, tmp_path):
+    """The INTEGRATION.md section 3 C example driven from a pure-C program
+    on device memory it allocates itself (cudaMalloc, the padded layout):
+    one_step (fast mode) within the fast tolerance of the oracle, and the
+    native time loop many_steps (exact mode, K steps) bit-identical to it."""
+    import numpy as np
+    from oracle import c_oracle
+    from oracle import sw_oracle as so
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = doc[doc.index("## 3. C / C++ callers"):]
+    snippet = sec[sec.index("```c") + 4:sec.index("```", sec.index("```c") + 4)]
+    c = tmp_path / "ex.c"
+    c.write_text(snippet + C_MAIN)
+    exe = tmp_path / "ex"
+    libdir = os.path.dirname(N.LIB_PATH)
+    cuda = "/usr/local/cuda"
+    subprocess.run(["gcc", "-O1", "-I", os.path.join(ROOT, "include"), "-I", f"{cuda}/include", str(c), "-o", str(exe),
+                    "-L", libdir, "-lfkc_sw", f"-Wl,-rpath,{libdir}", "-L", f"{cuda}/lib64", "-lcudart",
+                    f"-Wl,-rpath,{cuda}/lib64"], check=True)
+    H, U, V = so.random_state(nx, ny, "f32", seed=nx)
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        f.write(np.array([nx, ny, K], np.int32).tobytes())
+        for a in (H, U, V):
+            f.write(np.ascontiguousarray(a, np.float32).tobytes())
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(inp), str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    got = np.fromfile(out, np.float32).reshape(6, ny + 2, nx + 2)
+    one = so.step(H, U, V, 1.0, 1.0, 0.05)
+    for g, w in zip(got[:3], one):
+        assert np.max(np.abs(g.astype(np.float64) - w)) <= 2e-5 * np.max(np.abs(w))
+    want = c_oracle.run_fixed(H, U, V, K, 1.0, 1.0, 0.05)
+    for g, w in zip(got[3:], want):
+        assert np.array_equal(g, w)
