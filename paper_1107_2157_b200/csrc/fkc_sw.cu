@@ -13,6 +13,7 @@
 
 #include "../../include/fkc_sw.h"
 #include "sw_tma.cuh"
+#include "sw_resident.cuh"
 
 using namespace fkc;
 
@@ -399,6 +400,130 @@ int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
     return a->grid.dtype == FKC_F32 ? launch_tma_typed<float>(a, st) : launch_tma_typed<double>(a, st);
 }
 
+// ---------------------------------------------------------------------------
+// resident time loop (sw_resident.cuh): the whole loop of a small grid in one
+// cluster launch
+// ---------------------------------------------------------------------------
+// AUTO picks the resident loop for EAGER time loops (use_graph = 0: e.g.
+// swdemo.run) of grids up to these sizes, where it beats a launch per step
+// (B200, profiles/r02/resident.json: fast 128^2 2.8 vs 5.6 us / step eager,
+// 256^2 6.0 vs 4.8; exact 64^2 2.6, 128^2 7.2 vs 6.8).  Replayed CUDA graphs
+// (use_graph = 1, 2.3 us / step at 128^2) stay per-step.
+#ifndef FKC_RESIDENT_MAX_CELLS_FAST
+#define FKC_RESIDENT_MAX_CELLS_FAST (1 << 15)
+#endif
+#ifndef FKC_RESIDENT_MAX_CELLS_EXACT
+#define FKC_RESIDENT_MAX_CELLS_EXACT (1 << 13)
+#endif
+
+int smem_optin() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 227 * 1024;
+    if (cached[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cached[dev] = v > 0 ? v : 227 * 1024;
+    }
+    return cached[dev];
+}
+
+// cluster size and dynamic shared memory of the resident kernel for a grid
+// (0 = does not fit)
+struct ResPlan {
+    int nb;
+    size_t smem;
+};
+ResPlan plan_resident(const fkc_grid& g) {
+    const int es = g.dtype == FKC_F32 ? 4 : 8;
+    const size_t budget = (size_t)smem_optin() - 1024;   // static shared memory of the kernel
+    // as many CTAs (SMs) as the rows allow: a step's arithmetic is spread
+    // over the whole cluster (the cluster barrier costs the same)
+    const int nb = g.ny < RES_MAX_CLUSTER ? g.ny : RES_MAX_CLUSTER;
+    const int R = (g.ny + nb - 1) / nb;
+    const size_t bytes = (size_t)ResLayout(g.nx, R).n * 4 * es;   // 4-element records
+    if (bytes <= budget) return {nb, bytes};
+    return {0, 0};
+}
+
+template <class T, int DM>
+int launch_resident_t(const fkc_sw_loop_args* L, const ResPlan& rp, cudaStream_t st) {
+    auto kern = sw_resident<T, DM>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin() - 1024);
+        if (attr_err == cudaSuccess) attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    if (attr_err != cudaSuccess) return fail(FKC_ECUDA, "resident kernel attributes: %s", cudaGetErrorString(attr_err));
+    const fkc_sw_step_args& s = L->step;
+    ResArgs ra;
+    ra.nx = s.grid.nx; ra.ny = s.grid.ny; ra.pitch = s.grid.pitch;
+    const void* A[3] = {s.H, s.U, s.V};
+    void* B[3] = {s.oH, s.oU, s.oV};
+    const bool in_a = (L->first_step & 1) == 0;
+    const bool out_b = ((L->first_step + L->steps - 1) & 1) == 0;
+    for (int f = 0; f < 3; ++f) {
+        ra.in[f] = in_a ? A[f] : B[f];
+        ra.out[f] = out_b ? B[f] : (void*)A[f];
+    }
+    ra.dx = s.dx; ra.dy = s.dy; ra.g = s.g; ra.dt = s.dt; ra.cfl = s.cfl;
+    ra.dt_from_slots = L->dt_from_slots; ra.want_cfl = L->slots && L->want_cfl;
+    ra.bc = to_bcs(s.bc);
+    ra.first = L->first_step; ra.steps = L->steps;
+    ra.slots = (unsigned long long*)L->slots;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rp.nb);
+    cfg.blockDim = dim3(RES_THREADS);
+    cfg.dynamicSmemBytes = rp.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = rp.nb;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ra);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "sw_resident launch: %s", cudaGetErrorString(e));
+    if (L->slots && L->host_slots) {
+        e = cudaMemcpyAsync(L->host_slots + 5 * (L->first_step + 1), L->slots + 5 * (L->first_step + 1),
+                            5 * sizeof(uint64_t) * (size_t)L->steps, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (diagnostics rows): %s", cudaGetErrorString(e));
+    }
+    // row halos and corners of the final state (== apply_boundary of it, as the step kernels' fused epilogue)
+    return fkc_sw_apply_boundary(&s.grid, ra.out[0], ra.out[1], ra.out[2], s.bc, st);
+}
+
+// resident loop if asked for (variant RESIDENT) or, with AUTO, for small
+// grids that fit: returns -1 when the loop should take the per-step path
+int try_resident(const fkc_sw_loop_args* L, cudaStream_t st) {
+    const fkc_sw_step_args& s = L->step;
+    if (s.variant != FKC_VARIANT_RESIDENT && s.variant != FKC_VARIANT_AUTO) return -1;
+    const bool forced = s.variant == FKC_VARIANT_RESIDENT;
+    auto no = [&](const char* why) { return forced ? fail(FKC_EUSAGE, "resident variant: %s", why) : -1; };
+    if (!valid_grid(&s.grid)) return no("invalid grid");
+    if (!forced && (L->use_graph || (int64_t)s.grid.nx * s.grid.ny > (s.mode == FKC_MODE_FAST
+                                                                        ? FKC_RESIDENT_MAX_CELLS_FAST
+                                                                        : FKC_RESIDENT_MAX_CELLS_EXACT)))
+        return -1;
+    for (int i = 0; i < 4; ++i)
+        if (s.bc[i] != FKC_BC_REFLECTIVE && s.bc[i] != FKC_BC_PERIODIC) return no("reflective / periodic sides only");
+    if (!valid_bc(s.bc)) return no("invalid boundary spec");
+    if (s.mode != FKC_MODE_EXACT && s.mode != FKC_MODE_FAST) return no("invalid mode");
+    if (s.red.mass || s.red.max_abs_u || s.red.max_abs_v || s.red.cfl_min || s.red.err || s.dt_bound)
+        return no("per-call reductions / dt_bound: use slots");
+    if (!s.H || !s.U || !s.V || !s.oH || !s.oU || !s.oV) return no("null field pointer");
+    if (s.H == s.oH || s.U == s.oU || s.V == s.oV) return no("outputs alias inputs");
+    if (!(s.dx > 0) || !(s.dy > 0)) return no("dx, dy must be > 0");
+    const ResPlan rp = plan_resident(s.grid);
+    if (!rp.nb) return no("state does not fit in one cluster's shared memory");
+    const bool fast = s.mode == FKC_MODE_FAST;
+    if (s.grid.dtype == FKC_F32)
+        return fast ? launch_resident_t<float, DIV_FAST>(L, rp, st) : launch_resident_t<float, DIV_GUARD>(L, rp, st);
+    return fast ? launch_resident_t<double, DIV_FAST>(L, rp, st) : launch_resident_t<double, DIV_GUARD>(L, rp, st);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -478,6 +603,8 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
                                     "16-B aligned (fields and row peer lines)");
         return launch_tma(a, st);
     }
+    if (variant == FKC_VARIANT_RESIDENT)
+        return fail(FKC_EUSAGE, "the resident variant runs whole time loops (fkc_sw_advance_n)");
     if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");
     return a->grid.dtype == FKC_F32 ? launch_generic<float>(a, st) : launch_generic<double>(a, st);
 }
@@ -531,6 +658,10 @@ int fkc_sw_advance_n(const fkc_sw_loop_args* L, void* stream) {
     if (L->dt_from_slots && !L->slots) return fail(FKC_EUSAGE, "dt_from_slots needs slots");
     if (L->steps == 0) return FKC_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    {
+        const int rc = try_resident(L, st);
+        if (rc >= 0) return rc;
+    }
     if (!L->use_graph) return enqueue_loop(L, st);
     // graph path: key = the whole argument block (pointers, dt, steps, parity...)
     std::vector<unsigned char> key((const unsigned char*)L, (const unsigned char*)L + sizeof(*L));

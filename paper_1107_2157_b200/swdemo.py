@@ -32,7 +32,8 @@ from .region import Extent
 
 BC_CODES = {"reflective": N.BC_REFLECTIVE, "periodic": N.BC_PERIODIC, "none": N.BC_NONE}
 MODES = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}
-VARIANTS = {"auto": N.VARIANT_AUTO, "generic": N.VARIANT_GENERIC, "tma": N.VARIANT_TMA}
+VARIANTS = {"auto": N.VARIANT_AUTO, "generic": N.VARIANT_GENERIC, "tma": N.VARIANT_TMA,
+            "resident": N.VARIANT_RESIDENT}
 ENGINES = ("cuda",)
 
 
@@ -456,12 +457,20 @@ class Simulation:
         parity = self.n % 2
         L = self._loop_args(parity, steps, use_graph=True)
         sp = stream.cuda_stream
-        N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), sp))     # capture + first launch
-        self.n += steps
+        own = self.stream is None            # a private capture stream: order it with the caller's
+
+        def launch():
+            if own:
+                stream.wait_stream(torch.cuda.current_stream())
+            N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), sp))
+            if own:
+                torch.cuda.current_stream().wait_stream(stream)
+            self.n += steps
+
+        launch()                             # capture + first launch
 
         def replay():
-            N.check(N.lib().fkc_sw_advance_n(ctypes.byref(L), sp))
-            self.n += steps
+            launch()
         replay.args = L
         return replay
 
