@@ -20,7 +20,7 @@ FKC_OK, FKC_EDOMAIN, FKC_EUSAGE, FKC_ECUDA = 0, 1, 2, 3
 F32, F64 = 0, 1
 BC_REFLECTIVE, BC_PERIODIC, BC_NONE = 0, 1, 2
 MODE_EXACT, MODE_FAST = 0, 1
-VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA, VARIANT_RESIDENT = 0, 1, 2, 3
+VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA, VARIANT_RESIDENT, VARIANT_LOOP = 0, 1, 2, 3, 4
 ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG, ERR_NONPOSITIVE_FACE = 1, 2, 4, 8
 
 EXPORTS = (

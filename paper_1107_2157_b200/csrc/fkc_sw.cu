@@ -524,6 +524,147 @@ int try_resident(const fkc_sw_loop_args* L, cudaStream_t st) {
     return fast ? launch_resident_t<double, DIV_FAST>(L, rp, st) : launch_resident_t<double, DIV_GUARD>(L, rp, st);
 }
 
+// ---------------------------------------------------------------------------
+// persistent TMA time loop (sw_loop_tma): mid-size grids, one cooperative
+// launch for the whole loop
+// ---------------------------------------------------------------------------
+// Opt-in (variant LOOP); AUTO does not take it.  Measured on B200
+// (profiles/r02/loop_sweep.json, fast mode, fixed dt): 512^2 10.1 vs 4.3,
+// 1024^2 14.4 vs 9.9, 2048^2 38.5 vs 25.3 us / step against the per-step
+// kernels replayed from a CUDA graph -- even with the neighbour waits
+// compiled out (racy, timing only) a 1024^2 loop step takes 11.1 us: at
+// these sizes a warp's 12-row sweep at 8 resident warps per SM is latency
+// bound, and a per-step launch re-spreads the same work over 12-warp SMs
+// with short segments; from 4096^2 up the long per-warp sweeps also lose
+// DRAM efficiency (123 vs 73 us).  Kept as a correct, tested alternative
+// schedule (and for the CFL run without a host launch per step).
+// rows per warp segment of the persistent grid: every warp must be resident,
+// so the (bands x segments) CTAs fit in SMs x CTAs-per-SM; among the 4k-2
+// lengths (no wasted row in the last stage) the shortest that fits -- the
+// most warps sharing each step
+int loop_seg(int nbands, int ny, int64_t cap, const fkc_sw_tune& t) {
+    if (t.seg > 0) return t.seg;
+    for (int seg = 2; seg < ny + 4; seg += 4)
+        if ((int64_t)nbands * ((ny + seg - 1) / seg) <= cap) return seg;
+    return 0;
+}
+
+template <class T, bool FAST, int RED, int NW>
+int launch_loop_t(const fkc_sw_loop_args* L, cudaStream_t st, bool forced) {
+    using G = tma::Geo<T>;
+    using B = tma::Blk<T, NW>;
+    auto kern = sw_loop_tma<T, FAST, RED, NW>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    static int occ = 0;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM_BYTES);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, B::THREADS, B::SMEM_BYTES);
+    });
+    if (attr_err != cudaSuccess) return fail(FKC_ECUDA, "loop kernel attributes: %s", cudaGetErrorString(attr_err));
+    const fkc_sw_step_args& s = L->step;
+    const fkc_grid& g = s.grid;
+    const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
+    const int nbands = (nstrips + NW - 1) / NW;
+    const int64_t cap = (int64_t)sm_count() * occ;
+    const int seg = loop_seg(nbands, g.ny, cap, s.tune);
+    const int nseg = seg > 0 ? (g.ny + seg - 1) / seg : 0;
+    if (seg <= 0 || (int64_t)nbands * nseg > cap) {
+        if (!forced) return -1;
+        return fail(FKC_EUSAGE, "loop variant: %d x %d warps do not fit on the GPU at once (%lld CTAs)", nstrips,
+                    nseg, (long long)cap);
+    }
+    CUtensorMap m[6];
+    const void* ps[6] = {s.H, s.U, s.V, s.oH, s.oU, s.oV};
+    for (int f = 0; f < 6; ++f)
+        if (int rc = get_map(ps[f], g.nx, g.ny, g.pitch, G::BOXW, (int)sizeof(T), &m[f])) return rc;
+    const size_t nflags = (size_t)nseg * nstrips + 33;
+    uint32_t* ws = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&ws, nflags * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMallocAsync (loop flags): %s", cudaGetErrorString(e));
+    e = cudaMemsetAsync(ws, 0, nflags * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemsetAsync (loop flags): %s", cudaGetErrorString(e));
+    LoopBufs bufs{{(void*)s.H, (void*)s.U, (void*)s.V}, {s.oH, s.oU, s.oV}};
+    LoopCtl ctl;
+    ctl.first = L->first_step;
+    ctl.steps = L->steps;
+    ctl.slots = (unsigned long long*)L->slots;
+    ctl.dt_from_slots = L->dt_from_slots;
+    ctl.want_cfl = L->slots && L->want_cfl;
+    ctl.flags = ws;
+    ctl.bar = ws + (size_t)nseg * nstrips;
+    ctl.nstrips = nstrips;
+    ctl.per_lr = s.bc[0] == FKC_BC_PERIODIC;
+    ctl.per_du = s.bc[2] == FKC_BC_PERIODIC;
+    ctl.dt = s.dt;
+    ctl.cfl = s.cfl;
+    SegMap sm{seg, 0, 0, 0};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nbands, nseg);
+    cfg.blockDim = dim3(B::THREADS);
+    cfg.dynamicSmemBytes = B::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // every warp resident, or the launch fails
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, m[0], m[1], m[2], m[3], m[4], m[5], g.nx, g.ny, g.pitch, sm,
+                           s.tune.no_alternate ? 0 : 1, bufs, (T)s.dx, (T)s.dy, (T)s.g, to_bcs(s.bc), ctl);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(ws, st);
+        return fail(FKC_ECUDA, "sw_loop_tma launch: %s", cudaGetErrorString(e));
+    }
+    e = cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaFreeAsync (loop flags): %s", cudaGetErrorString(e));
+    if (L->slots && L->host_slots) {
+        e = cudaMemcpyAsync(L->host_slots + 5 * (L->first_step + 1), L->slots + 5 * (L->first_step + 1),
+                            5 * sizeof(uint64_t) * (size_t)L->steps, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (diagnostics rows): %s", cudaGetErrorString(e));
+    }
+    return FKC_OK;
+}
+
+template <class T, bool FAST, int RED>
+int launch_loop_nw(const fkc_sw_loop_args* L, cudaStream_t st, bool forced) {
+    if (L->step.tune.warps > 1) return fail(FKC_EUSAGE, "loop variant: one warp per CTA (tune.warps 0 or 1)");
+    return launch_loop_t<T, FAST, RED, 1>(L, st, forced);
+}
+
+template <class T>
+int launch_loop_typed(const fkc_sw_loop_args* L, cudaStream_t st, bool forced) {
+    const bool fast = L->step.mode == FKC_MODE_FAST;
+    const int lvl = L->slots ? (L->want_cfl ? 2 : 1) : 0;
+    if (fast) {
+        if (lvl == 2) return launch_loop_nw<T, true, 2>(L, st, forced);
+        return lvl ? launch_loop_nw<T, true, 1>(L, st, forced) : launch_loop_nw<T, true, 0>(L, st, forced);
+    }
+    if (lvl == 2) return launch_loop_nw<T, false, 2>(L, st, forced);
+    return lvl ? launch_loop_nw<T, false, 1>(L, st, forced) : launch_loop_nw<T, false, 0>(L, st, forced);
+}
+
+// persistent loop if asked for (variant LOOP) or, with AUTO, for mid-size
+// grids: returns -1 when the loop should take another path
+int try_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
+    const fkc_sw_step_args& s = L->step;
+    if (s.variant != FKC_VARIANT_LOOP && s.variant != FKC_VARIANT_AUTO) return -1;
+    const bool forced = s.variant == FKC_VARIANT_LOOP;
+    auto no = [&](const char* why) { return forced ? fail(FKC_EUSAGE, "loop variant: %s", why) : -1; };
+    if (!valid_grid(&s.grid)) return no("invalid grid");
+    if (!forced) return -1;
+    if (!valid_bc(s.bc)) return no("invalid boundary spec");
+    if (s.mode != FKC_MODE_EXACT && s.mode != FKC_MODE_FAST) return no("invalid mode");
+    if (s.red.mass || s.red.max_abs_u || s.red.max_abs_v || s.red.cfl_min || s.red.err || s.dt_bound)
+        return no("per-call reductions / dt_bound: use slots");
+    if (!s.H || !s.U || !s.V || !s.oH || !s.oU || !s.oV) return no("null field pointer");
+    if (s.H == s.oH || s.U == s.oU || s.V == s.oV) return no("outputs alias inputs");
+    if (!(s.dx > 0) || !(s.dy > 0)) return no("dx, dy must be > 0");
+    if (int rc = valid_tune(s.tune)) return rc;
+    if (!tma_eligible(&s)) return no("needs the TMA layout (nx, pitch multiples of 16 / element size, aligned fields)");
+    return s.grid.dtype == FKC_F32 ? launch_loop_typed<float>(L, st, forced) : launch_loop_typed<double>(L, st, forced);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -603,8 +744,8 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
                                     "16-B aligned (fields and row peer lines)");
         return launch_tma(a, st);
     }
-    if (variant == FKC_VARIANT_RESIDENT)
-        return fail(FKC_EUSAGE, "the resident variant runs whole time loops (fkc_sw_advance_n)");
+    if (variant == FKC_VARIANT_RESIDENT || variant == FKC_VARIANT_LOOP)
+        return fail(FKC_EUSAGE, "the resident / loop variants run whole time loops (fkc_sw_advance_n)");
     if (variant != FKC_VARIANT_GENERIC) return fail(FKC_EUSAGE, "invalid variant");
     return a->grid.dtype == FKC_F32 ? launch_generic<float>(a, st) : launch_generic<double>(a, st);
 }
@@ -660,6 +801,10 @@ int fkc_sw_advance_n(const fkc_sw_loop_args* L, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     {
         const int rc = try_resident(L, st);
+        if (rc >= 0) return rc;
+    }
+    {
+        const int rc = try_loop(L, st);
         if (rc >= 0) return rc;
     }
     if (!L->use_graph) return enqueue_loop(L, st);

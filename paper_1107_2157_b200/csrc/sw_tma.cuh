@@ -313,26 +313,90 @@ __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int
     }
 }
 
+// Persistent time loop (sw_loop_tma below): control block and the
+// neighbour ordering between its steps.
+// a loop has no peer tiles (zero-initialised constant bank: no local copy)
+__constant__ Peers c_no_peers;
+__constant__ SyncArgs c_no_sync;
+struct LoopBufs {
+    void* a[3];      // buffer A (H, U, V): the input of even global steps
+    void* b[3];      // buffer B
+};
+struct LoopCtl {
+    int64_t first, steps;
+    unsigned long long* slots;   // 5 words per state row, or null
+    int dt_from_slots, want_cfl;
+    uint32_t* flags;             // per warp: steps completed (zeroed), index seg * nstrips + strip
+    uint32_t* bar;               // 32 arrival sub-counters + 1 top counter (zeroed; CFL mode)
+    int nstrips;
+    int per_lr, per_du;          // periodic left / right, down / up
+    double dt, cfl;
+};
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Poll with relaxed loads (an ld.acquire compiles to an L1 invalidate per
+// poll -- measured: 28 % of the loop's stall samples), then one acquire
+// fence once the counter is reached.
+__device__ __forceinline__ void spin_until(const uint32_t* p, uint32_t target, uint32_t* err) {
+    if ((int32_t)(ld_relaxed_gpu(p) - target) < 0) {
+        const long long t0 = clock64();
+        while ((int32_t)(ld_relaxed_gpu(p) - target) < 0) {
+            __nanosleep(32);
+            if (clock64() - t0 > 4000000000ll) watchdog_fire(err);
+        }
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// Before a loop step's first load: lanes 0..3 each wait (acquire, gpu
+// scope) until one direct neighbour warp -- left / right strip of the
+// segment, segment below / above in the strip, the periodic wrap partners
+// at the domain edges -- completed `target` steps; the four polls run in
+// parallel and __syncwarp orders them before lane 0's TMA issue.
+// Neighbours are re-derived here (a few integer ops once per step) rather
+// than kept in registers across the sweep.
+__device__ __forceinline__ void loop_nbr_wait(const LoopCtl& c, int strip, uint32_t target, int lane, uint32_t* err) {
+    if (lane < 4) {
+        const int ns = c.nstrips, seg = (int)blockIdx.y, nseg = (int)gridDim.y;
+        int sg = seg, st = strip;
+        if (lane == 0) st = strip > 0 ? strip - 1 : (c.per_lr ? ns - 1 : strip);
+        else if (lane == 1) st = strip < ns - 1 ? strip + 1 : (c.per_lr ? 0 : strip);
+        else if (lane == 2) sg = seg > 0 ? seg - 1 : (c.per_du ? nseg - 1 : seg);
+        else sg = seg < nseg - 1 ? seg + 1 : (c.per_du ? 0 : seg);
+        if (sg != seg || st != strip) spin_until(c.flags + sg * ns + st, target, err);
+    }
+    __syncwarp();
+}
+
 // Tensor coordinates: the maps are encoded with base = &field(1 - CPL, 0)
 // so that full-array column x is tensor column x + CPL - 1 (16-B aligned
 // boxes: cell 1 is 128-B aligned).  Strip j owns columns
 // [1 + OWN j, OWN (j+1)] and loads full columns [1 + OWN j - CPL,
 // OWN (j+1) + CPL] (ghost lanes 0 and 31 on either side).
+//
+// One warp's sweep of its (strip, row segment) for one step: the body of
+// the step kernel sw_step_tma, and of every step of the persistent loop
+// sw_loop_tma.  `kb` = ring stages the warp consumed before (mbarrier slot
+// and phase continue across the steps of a loop); returns the stages this
+// sweep consumed (0: the strip owns nothing).
 template <class T, bool FAST, int RED, int NW>
-__global__ void __launch_bounds__(NW * 32, tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>())
-sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
-            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, SegMap sm, int alt,
-            T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
-            T dx, T dy, DtSrc dts, T g, const __grid_constant__ BCs bc, RedPtrs red,
-            const __grid_constant__ Peers P, SyncArgs sy) {
+__device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorMap* tmU, const CUtensorMap* tmV,
+                                         int nx, int ny, int64_t pitch, const SegMap& sm, int alt,
+                                         T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV, T dx, T dy,
+                                         const DtSrc& dts, T g, const BCs& bc, const RedPtrs& red, const Peers& P,
+                                         const SyncArgs& sy, uint32_t sbase, uint32_t kb,
+                                         const LoopCtl* lc = nullptr, uint32_t target = 0u) {
     using namespace tma;
     using G = Geo<T>;
     constexpr int CPL = G::CPL;
     // one 16-byte vector per lane keeps every TMA box start (tensor column
     // OWN j, i.e. 480 j bytes) 16-byte aligned
     constexpr int DM = FAST ? DIV_FAST : DIV_GUARD;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -340,7 +404,7 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
     const int txl = xs + G::LEAD;                        // its tensor column
     const int tx = G::VEC == 16 ? txl : (txl & ~1);      // box start (16-B aligned)
-    if (xs + CPL > nx) return;                           // strip owns nothing (ragged last band)
+    if (xs + CPL > nx) return 0;                         // strip owns nothing (ragged last band)
     int y0, nrows;                                       // first interior row of the segment, rows
     seg_rows(sm, blockIdx.y, ny, y0, nrows);
     const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
@@ -371,20 +435,23 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         if (strip == 0) sides |= 1u << SIDE_L;
         if (G::OWN * (strip + 1) >= nx) sides |= 1u << SIDE_R;
     }
-    pdl_launch_dependents();
-    if (lane == 0) {
-        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();                                 // the barriers are initialised before any lane uses them
-    pdl_wait();                                   // the previous step's output is complete
+#ifndef FKC_LOOP_NOWAIT
+#define FKC_LOOP_NOWAIT 0     // timing experiments only (racy): skip the neighbour waits
+#endif
+    if (lc && !FKC_LOOP_NOWAIT) loop_nbr_wait(*lc, strip, target, lane, red.err);
     if (lane == 0) {
         if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
-        for (int k = 0; k < tma::S - 1 && k < nstages; ++k)
-            issue_stage<T>(ring + k * G::STAGE_BYTES, full + 8 * k, &tmH, &tmU, &tmV, tx, stage_y(k));
+        // the neighbours' generic-proxy stores are read by TMA (async proxy)
+        if (lc) asm volatile("fence.proxy.async.global;" ::: "memory");
+        // ring slots are free: the previous sweep's generic reads of them are
+        // ordered before the new TMA writes
+        if (kb) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int k = 0; k < tma::S - 1 && k < nstages; ++k) {
+            const uint32_t sl = (kb + k) % tma::S;
+            issue_stage<T>(ring + sl * G::STAGE_BYTES, full + 8 * sl, tmH, tmU, tmV, tx, stage_y(k));
+        }
     }
     __syncwarp();
-
     const T dt = resolve_dt<T>(dts);
     const Coef<T> c = make_coef<T>(dx, dy, dt, g);
     const T dmin = dx < dy ? dx : dy;
@@ -454,15 +521,16 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         return k < (nr + 2 + R - 1) / R;
     };
     for (int k = 0; stages_left(k); ++k) {
-        const int s = k % tma::S;
+        const uint32_t kg = kb + (uint32_t)k;          // ring stage index over the warp's lifetime
+        const int s = (int)(kg % tma::S);
         // refill the slot freed by stage k-1 (every lane finished reading it)
         if (lane == 0 && k + tma::S - 1 < nstages) {
             const int kn = k + tma::S - 1;
+            const uint32_t sl = (kb + (uint32_t)kn) % tma::S;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_stage<T>(ring + (kn % tma::S) * G::STAGE_BYTES, full + 8 * (kn % tma::S), &tmH, &tmU, &tmV, tx,
-                             stage_y(kn));
+            issue_stage<T>(ring + sl * G::STAGE_BYTES, full + 8 * sl, tmH, tmU, tmV, tx, stage_y(kn));
         }
-        mbar_wait(full + 8 * s, (k / tma::S) & 1, red.err);
+        mbar_wait(full + 8 * s, (kg / tma::S) & 1, red.err);
         // cells whose loaded data is not part of the grid become a lake at
         // rest IN SHARED MEMORY (the lane's own 16-B slots of the stage, read
         // back by the same lane: program order suffices; the slot's next TMA
@@ -599,6 +667,126 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
         if (lane == 0) peer_signal(sy, sides, expected);
     }
     if constexpr (RED > 0) rr.commit(red, lane, dmin, fdep);
+    return nstages;
+}
+
+// One time step: every warp sweeps its (strip, segment) once.
+template <class T, bool FAST, int RED, int NW>
+__global__ void __launch_bounds__(NW * 32, tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>())
+sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
+            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, SegMap sm, int alt,
+            T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
+            T dx, T dy, DtSrc dts, T g, const __grid_constant__ BCs bc, RedPtrs red,
+            const __grid_constant__ Peers P, SyncArgs sy) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
+    pdl_launch_dependents();
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();                                 // the barriers are initialised before any lane uses them
+    pdl_wait();                                   // the previous step's output is complete
+    tma_sweep<T, FAST, RED, NW>(&tmH, &tmU, &tmV, nx, ny, pitch, sm, alt, oH, oU, oV, dx, dy, dts, g, bc, red, P, sy,
+                                sbase, 0u);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent time loop (mid-size grids, fkc_sw_advance_n): the step grid is
+// launched ONCE (cooperatively: every warp resident) and each warp sweeps
+// the same (strip, segment) step after step.  Between steps a warp waits
+// only for its direct neighbours -- left / right strips of its segment,
+// segments below / above in its strip, and the periodic wrap partners,
+// i.e. every warp whose cells it reads (its loaded columns and halo rows)
+// or whose reads of the buffer it is about to overwrite it must not race
+// (double buffering: step s+1 overwrites state s-1) -- through per-warp
+// step counters in global memory (release / acquire).  Cells of the
+// diagonal neighbours that the TMA boxes bring in (ghost lanes of the halo
+// rows) feed no stored value.  With a CFL-chosen dt every step ends in a
+// grid-wide arrival (two-level counters) so the next dt sees every warp's
+// bound.  No launch per step, no tail wave, the state stays in L2.
+// ---------------------------------------------------------------------------
+// f32 fast mode: the loop's extra live state does not fit the step
+// kernel's 168-register budget (12 warps per SM) without spills; the loop
+// kernel runs FKC_LOOP_WARPS_FAST warps per SM instead (registers are split
+// over the 4 SM sub-partitions: 9-12 warps cap a warp at 168, 8 at 255)
+#ifndef FKC_LOOP_WARPS_FAST
+#define FKC_LOOP_WARPS_FAST 8
+#endif
+template <class T, bool FAST, int RED, int NW>
+constexpr int loop_ctas_per_sm() {
+    return (FAST && sizeof(T) == 4) ? (FKC_LOOP_WARPS_FAST / NW > 0 ? FKC_LOOP_WARPS_FAST / NW : 1)
+                                    : tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>();
+}
+template <class T, bool FAST, int RED, int NW>
+__global__ void __launch_bounds__(NW * 32, (loop_ctas_per_sm<T, FAST, RED, NW>()))
+sw_loop_tma(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+            const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mB0,
+            const __grid_constant__ CUtensorMap mB1, const __grid_constant__ CUtensorMap mB2, int nx, int ny,
+            int64_t pitch, SegMap sm, int alt, const __grid_constant__ LoopBufs bufs, T dx, T dy, T g,
+            const __grid_constant__ BCs bc, const __grid_constant__ LoopCtl ctl) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
+    const int strip = blockIdx.x * NW + warp;
+    if (strip >= ctl.nstrips) return;               // owns nothing (no neighbour waits on it)
+    if (lane == 0) {
+        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int nseg = (int)gridDim.y, ns = ctl.nstrips;
+    const int me = (int)blockIdx.y * ns + strip;
+    // grid-wide arrival (CFL mode): warp `me` arrives on sub-counter me % 32
+    const int nwarps = nseg * ns;
+    const int nsub = nwarps < 32 ? nwarps : 32;
+    const uint32_t sub_n = (uint32_t)(nwarps / 32 + ((me % 32) < (nwarps % 32) ? 1 : 0));
+    const bool cfl_loop = ctl.dt_from_slots != 0;
+    uint32_t kb = 0;
+    for (int64_t s = 0; s < ctl.steps; ++s) {
+        const int64_t i = ctl.first + s;
+        const bool even = (i & 1) == 0;
+        const CUtensorMap* m0 = even ? &mA0 : &mB0;
+        const CUtensorMap* m1 = even ? &mA1 : &mB1;
+        const CUtensorMap* m2 = even ? &mA2 : &mB2;
+        void* const* out = even ? bufs.b : bufs.a;
+        DtSrc dts{ctl.dt, nullptr, ctl.cfl};
+        RedPtrs red{nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (ctl.slots) {
+            unsigned long long* row = ctl.slots + 5 * (i + 1);
+            red = RedPtrs{(double*)row, row + 1, row + 2, ctl.want_cfl ? row + 3 : nullptr, (uint32_t*)(row + 4)};
+            if (cfl_loop) dts.bound = ctl.slots + 5 * i + 3;
+        }
+        const int n = tma_sweep<T, FAST, RED, NW>(m0, m1, m2, nx, ny, pitch, sm, alt, (T*)out[0], (T*)out[1],
+                                                  (T*)out[2], dx, dy, dts, g, bc, red, c_no_peers, c_no_sync, sbase, kb,
+                                                  (s > 0 && !cfl_loop) ? &ctl : nullptr, (uint32_t)s);
+        kb += (uint32_t)n;
+        __syncwarp();                                // every lane's stores (and reduction atomics) issued
+        if (lane == 0) {
+#ifndef FKC_LOOP_WRITER_PROXY
+#define FKC_LOOP_WRITER_PROXY 1
+#endif
+            if (FKC_LOOP_WRITER_PROXY) asm volatile("fence.proxy.async.global;" ::: "memory");   // our stores, read by TMA next
+            if (cfl_loop) {
+                __threadfence();
+                // grid-wide arrival: the last warp of a sub-counter bumps the top
+                const uint32_t old = atomicAdd(ctl.bar + (me % 32), 1u);
+                if (old + 1u == sub_n * (uint32_t)(s + 1)) {
+                    __threadfence();
+                    atomicAdd(ctl.bar + 32, 1u);
+                }
+                spin_until(ctl.bar + 32, (uint32_t)nsub * (uint32_t)(s + 1), red.err);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            } else {
+                st_release_gpu(ctl.flags + me, (uint32_t)(s + 1));
+            }
+        }
+        __syncwarp();
+    }
 }
 
 }  // namespace fkc

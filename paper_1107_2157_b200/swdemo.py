@@ -33,7 +33,7 @@ from .region import Extent
 BC_CODES = {"reflective": N.BC_REFLECTIVE, "periodic": N.BC_PERIODIC, "none": N.BC_NONE}
 MODES = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}
 VARIANTS = {"auto": N.VARIANT_AUTO, "generic": N.VARIANT_GENERIC, "tma": N.VARIANT_TMA,
-            "resident": N.VARIANT_RESIDENT}
+            "resident": N.VARIANT_RESIDENT, "loop": N.VARIANT_LOOP}
 ENGINES = ("cuda",)
 
 
