@@ -404,16 +404,23 @@ int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
 // resident time loop (sw_resident.cuh): the whole loop of a small grid in one
 // cluster launch
 // ---------------------------------------------------------------------------
-// AUTO picks the resident loop for EAGER time loops (use_graph = 0: e.g.
-// swdemo.run) of grids up to these sizes, where it beats a launch per step
-// (B200, profiles/r02/resident.json: fast 128^2 2.8 vs 5.6 us / step eager,
-// 256^2 6.0 vs 4.8; exact 64^2 2.6, 128^2 7.2 vs 6.8).  Replayed CUDA graphs
-// (use_graph = 1, 2.3 us / step at 128^2) stay per-step.
-#ifndef FKC_RESIDENT_MAX_CELLS_FAST
-#define FKC_RESIDENT_MAX_CELLS_FAST (1 << 15)
+// AUTO picks the resident loop for time loops (eager or captured in a
+// graph) of grids up to these sizes that fit one cluster's shared memory.
+// B200 (profiles/r02/resident_sweep.json, us / step, resident vs the best
+// per-step kernel replayed from a CUDA graph): f32 fast 64^2 1.16 vs 2.34,
+// 128^2 1.92 vs 2.64, 224^2 2.64 vs 2.76, 256^2 4.29 vs 2.77 (three strips
+// of 8 warps); f32 exact 128^2 3.16 vs 3.86, 224^2 4.71 vs 5.52, 256^2 6.37
+// vs 5.45; f64 exact 160^2 5.40 vs 6.80; f64 fast 96^2 1.93 vs 2.84, 128^2
+// 2.88 vs 2.88.  The SPEC run (CFL dt + diagnostics, eager): 128^2 3.29 vs
+// 6.15 (fast), 4.86 vs 6.72 (exact).
+#ifndef FKC_RESIDENT_MAX_CELLS_F32
+#define FKC_RESIDENT_MAX_CELLS_F32 (224 * 224)
 #endif
-#ifndef FKC_RESIDENT_MAX_CELLS_EXACT
-#define FKC_RESIDENT_MAX_CELLS_EXACT (1 << 13)
+#ifndef FKC_RESIDENT_MAX_CELLS_F64_FAST
+#define FKC_RESIDENT_MAX_CELLS_F64_FAST (112 * 112)
+#endif
+#ifndef FKC_RESIDENT_MAX_CELLS_F64_EXACT
+#define FKC_RESIDENT_MAX_CELLS_F64_EXACT (160 * 160)
 #endif
 
 int smem_optin() {
@@ -428,27 +435,38 @@ int smem_optin() {
     return cached[dev];
 }
 
-// cluster size and dynamic shared memory of the resident kernel for a grid
-// (0 = does not fit)
+// cluster size, warps and dynamic shared memory of the resident kernel for
+// a grid (nb = 0: does not fit one cluster's shared memory)
 struct ResPlan {
-    int nb;
+    int nb, groups, warps;
     size_t smem;
 };
-ResPlan plan_resident(const fkc_grid& g) {
-    const int es = g.dtype == FKC_F32 ? 4 : 8;
+template <class T>
+ResPlan plan_resident_t(const fkc_grid& g, bool fast) {
     const size_t budget = (size_t)smem_optin() - 1024;   // static shared memory of the kernel
     // as many CTAs (SMs) as the rows allow: a step's arithmetic is spread
     // over the whole cluster (the cluster barrier costs the same)
     const int nb = g.ny < RES_MAX_CLUSTER ? g.ny : RES_MAX_CLUSTER;
     const int R = (g.ny + nb - 1) / nb;
-    const size_t bytes = (size_t)ResLayout(g.nx, R).n * 4 * es;   // 4-element records
-    if (bytes <= budget) return {nb, bytes};
-    return {0, 0};
+    const ResGeo<T> geo(g.nx, R);
+    if (geo.bytes() > budget) return {0, 0, 0, 0};
+    // row groups: ~FKC_RES_GROUP_ROWS_* rows per warp's sweep (2 halo rows of
+    // overhead each), at most res_warps() warps per CTA
+    const int grows = fast ? FKC_RES_GROUP_ROWS_FAST : FKC_RES_GROUP_ROWS_EXACT;
+    int groups = (R + grows - 1) / grows;
+    const int gmax = (fast ? res_warps<T, true>() : res_warps<T, false>()) / geo.ns;
+    if (gmax < 1) return {0, 0, 0, 0};
+    if (groups > gmax) groups = gmax;
+    if (groups < 1) groups = 1;
+    return {nb, groups, groups * geo.ns, geo.bytes()};
+}
+ResPlan plan_resident(const fkc_grid& g, bool fast) {
+    return g.dtype == FKC_F32 ? plan_resident_t<float>(g, fast) : plan_resident_t<double>(g, fast);
 }
 
-template <class T, int DM>
+template <class T, bool FAST, int RED>
 int launch_resident_t(const fkc_sw_loop_args* L, const ResPlan& rp, cudaStream_t st) {
-    auto kern = sw_resident<T, DM>;
+    auto kern = sw_resident<T, FAST, RED>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -472,9 +490,10 @@ int launch_resident_t(const fkc_sw_loop_args* L, const ResPlan& rp, cudaStream_t
     ra.bc = to_bcs(s.bc);
     ra.first = L->first_step; ra.steps = L->steps;
     ra.slots = (unsigned long long*)L->slots;
+    ra.groups = rp.groups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(rp.nb);
-    cfg.blockDim = dim3(RES_THREADS);
+    cfg.blockDim = dim3(rp.warps * 32);
     cfg.dynamicSmemBytes = rp.smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -495,6 +514,13 @@ int launch_resident_t(const fkc_sw_loop_args* L, const ResPlan& rp, cudaStream_t
     return fkc_sw_apply_boundary(&s.grid, ra.out[0], ra.out[1], ra.out[2], s.bc, st);
 }
 
+template <class T, bool FAST>
+int launch_resident_red(const fkc_sw_loop_args* L, const ResPlan& rp, cudaStream_t st) {
+    if (!L->slots) return launch_resident_t<T, FAST, 0>(L, rp, st);
+    if (L->want_cfl || L->dt_from_slots) return launch_resident_t<T, FAST, 2>(L, rp, st);
+    return launch_resident_t<T, FAST, 1>(L, rp, st);
+}
+
 // resident loop if asked for (variant RESIDENT) or, with AUTO, for small
 // grids that fit: returns -1 when the loop should take the per-step path
 int try_resident(const fkc_sw_loop_args* L, cudaStream_t st) {
@@ -503,10 +529,10 @@ int try_resident(const fkc_sw_loop_args* L, cudaStream_t st) {
     const bool forced = s.variant == FKC_VARIANT_RESIDENT;
     auto no = [&](const char* why) { return forced ? fail(FKC_EUSAGE, "resident variant: %s", why) : -1; };
     if (!valid_grid(&s.grid)) return no("invalid grid");
-    if (!forced && (L->use_graph || (int64_t)s.grid.nx * s.grid.ny > (s.mode == FKC_MODE_FAST
-                                                                        ? FKC_RESIDENT_MAX_CELLS_FAST
-                                                                        : FKC_RESIDENT_MAX_CELLS_EXACT)))
-        return -1;
+    const int64_t max_cells = s.grid.dtype == FKC_F32 ? FKC_RESIDENT_MAX_CELLS_F32
+                              : (s.mode == FKC_MODE_FAST ? FKC_RESIDENT_MAX_CELLS_F64_FAST
+                                                         : FKC_RESIDENT_MAX_CELLS_F64_EXACT);
+    if (!forced && (int64_t)s.grid.nx * s.grid.ny > max_cells) return -1;
     for (int i = 0; i < 4; ++i)
         if (s.bc[i] != FKC_BC_REFLECTIVE && s.bc[i] != FKC_BC_PERIODIC) return no("reflective / periodic sides only");
     if (!valid_bc(s.bc)) return no("invalid boundary spec");
@@ -516,12 +542,14 @@ int try_resident(const fkc_sw_loop_args* L, cudaStream_t st) {
     if (!s.H || !s.U || !s.V || !s.oH || !s.oU || !s.oV) return no("null field pointer");
     if (s.H == s.oH || s.U == s.oU || s.V == s.oV) return no("outputs alias inputs");
     if (!(s.dx > 0) || !(s.dy > 0)) return no("dx, dy must be > 0");
-    const ResPlan rp = plan_resident(s.grid);
+    const int cpl = s.grid.dtype == FKC_F32 ? 4 : 2;
+    if (s.grid.nx % cpl != 0) return no("nx must be a multiple of 16 / element size (the row engines' lane vectors)");
+    const ResPlan rp = plan_resident(s.grid, s.mode == FKC_MODE_FAST);
     if (!rp.nb) return no("state does not fit in one cluster's shared memory");
     const bool fast = s.mode == FKC_MODE_FAST;
     if (s.grid.dtype == FKC_F32)
-        return fast ? launch_resident_t<float, DIV_FAST>(L, rp, st) : launch_resident_t<float, DIV_GUARD>(L, rp, st);
-    return fast ? launch_resident_t<double, DIV_FAST>(L, rp, st) : launch_resident_t<double, DIV_GUARD>(L, rp, st);
+        return fast ? launch_resident_red<float, true>(L, rp, st) : launch_resident_red<float, false>(L, rp, st);
+    return fast ? launch_resident_red<double, true>(L, rp, st) : launch_resident_red<double, false>(L, rp, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -46,7 +46,7 @@ def test_config1_golden_run_resident():
     assert np.max(np.abs(rows[:, 3] - g["rows"][:, 3]) / g["rows"][:, 3]) <= 1e-12
 
 
-@pytest.mark.parametrize("nx,ny", [(128, 128), (64, 200), (37, 53), (1, 5), (300, 7), (200, 17)])
+@pytest.mark.parametrize("nx,ny", [(128, 128), (64, 200), (36, 53), (4, 5), (300, 7), (200, 17), (124, 1), (240, 31)])
 @pytest.mark.parametrize("bc", ["reflective", "periodic"])
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 def test_resident_exact_fixed_dt(nx, ny, bc, prec):
@@ -104,9 +104,9 @@ def test_resident_fast_within_tolerance(n):
 
 
 def test_auto_picks_resident_for_small_grids_and_graph_replay():
-    """AUTO runs small grids' eager loops resident (one launch for the whole
-    loop) -- the results equal the per-step path's -- and Simulation.capture's
-    graph replays (per-step kernels) keep advancing the state."""
+    """AUTO runs small grids' loops resident (one launch for the whole loop,
+    eager or inside Simulation.capture's graph) -- the results equal the
+    per-step path's -- and graph replays keep advancing the state."""
     from paper_1107_2157_b200 import swdemo
     H, U, V = so.random_state(128, 128, "f32", seed=3)
     outs = []
@@ -147,3 +147,37 @@ def test_resident_errors():
     big = swdemo.SWConfig(nx=2048, ny=2048, steps=2, dt=0.05, variant="resident")
     with pytest.raises(swdemo.LaunchError):
         swdemo.run(big)
+    # the row engines' lane vectors: nx a multiple of 4 (f32) / 2 (f64)
+    odd = swdemo.SWConfig(nx=37, ny=40, steps=2, dt=0.05, variant="resident")
+    with pytest.raises(swdemo.LaunchError):
+        swdemo.run(odd)
+
+
+@pytest.mark.parametrize("n,prec", [(256, "f32"), (352, "f32"), (160, "f64")])
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_resident_largest_grids(n, prec, mode):
+    """The largest grids one cluster holds (256^2 - 352^2 f32, 160^2 f64):
+    exact bit-identical to the oracle, fast within tolerance, 12 steps."""
+    from paper_1107_2157_b200 import swdemo
+    H, U, V = so.random_state(n, n, prec, seed=n + 11)
+    want = c_oracle.run_fixed(H, U, V, 12, 1.0, 1.0, 0.05)
+    cfg = swdemo.SWConfig(nx=n, ny=n, steps=12, dt=0.05, mode=mode, precision=prec, variant="resident")
+    sim = swdemo.Simulation(cfg, state=dev_state(H, U, V), diagnostics=False)
+    sim.advance(12)
+    for x, w in zip(host(sim.state()), want):
+        if mode == "exact":
+            assert np.array_equal(x, w)
+        else:
+            assert np.max(np.abs(x.astype(np.float64) - w)) <= FAST_RTOL * np.max(np.abs(w))
+
+
+def test_auto_falls_back_for_unaligned_width():
+    """AUTO runs a small grid whose width the row engines cannot take
+    (nx % 4 != 0) on the per-step generic kernel -- same bits."""
+    from paper_1107_2157_b200 import swdemo
+    H, U, V = so.random_state(37, 29, "f32", seed=2)
+    want = c_oracle.run_fixed(H, U, V, 5, 1.0, 1.0, 0.05)
+    cfg = swdemo.SWConfig(nx=37, ny=29, steps=5, dt=0.05)
+    sim = swdemo.Simulation(cfg, state=dev_state(H, U, V), diagnostics=False)
+    sim.advance(5)
+    assert all(np.array_equal(x, w) for x, w in zip(host(sim.state()), want))
