@@ -24,7 +24,7 @@ VARIANT_AUTO, VARIANT_GENERIC, VARIANT_TMA, VARIANT_RESIDENT, VARIANT_LOOP = 0, 
 ERR_NONPOSITIVE_DEPTH, ERR_NONFINITE, ERR_WATCHDOG, ERR_NONPOSITIVE_FACE = 1, 2, 4, 8
 
 EXPORTS = (
-    "fkc_sw_step", "fkc_sw_advance_n", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
+    "fkc_sw_step", "fkc_sw_advance_n", "fkc_sw_run_host", "fkc_sw_apply_boundary", "fkc_sw_reduce_state", "fkc_sw_reduce_reset",
     "fkc_region_cpy", "fkc_cshift", "fkc_copy2d", "fkc_halo_pack", "fkc_halo_unpack",
     "fkc_ipc_export", "fkc_ipc_open", "fkc_ipc_close",
     "fkc_tma_plan", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_test_sqrt2_f32", "fkc_last_error",
@@ -135,6 +135,7 @@ def lib():
     sig = {
         "fkc_sw_step": [ctypes.POINTER(StepArgs), vp],
         "fkc_sw_advance_n": [ctypes.POINTER(LoopArgs), vp],
+        "fkc_sw_run_host": [ctypes.POINTER(LoopArgs), ctypes.POINTER(vp), ctypes.POINTER(vp), i64, i32, vp],
         "fkc_sw_apply_boundary": [ctypes.POINTER(Grid), vp, vp, vp, ctypes.POINTER(i32), vp],
         "fkc_sw_reduce_state": [ctypes.POINTER(Grid), vp, vp, vp, dbl, dbl, dbl,
                                 ctypes.POINTER(Reduce), vp],

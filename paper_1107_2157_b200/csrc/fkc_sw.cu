@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -298,7 +299,7 @@ int seg_rev(const fkc_sw_tune& t) {
 // Guided segmentation: the last ~tail_waves waves of CTAs get short
 // segments of `tail` rows.
 SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
-    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t), 0, 0, 0};
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t), 0, 0, 0, 1, ny};
     // auto: about half the segment, again 4k - 2 rows (30 -> 14, 22 -> 10, 14 -> 6, 10 / 6 -> 2)
     const int tail = t.tail_rows == 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : t.tail_rows;
     if (tail <= 0 || tail >= m.seg || t.seg > 0) return m;
@@ -328,8 +329,9 @@ TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_
     return p;
 }
 
+// Row window [ybase, ybase + nyw) of the interior (nyw 0: all rows).
 template <class T, bool FAST, int RED, int NW>
-int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
+int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m, int ybase, int nyw) {
     using G = tma::Geo<T>;
     using B = tma::Blk<T, NW>;
     auto kern = sw_step_tma<T, FAST, RED, NW>;
@@ -341,8 +343,10 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     if (attr_err != cudaSuccess)
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
-    TmaPlan p = plan_tma(g.nx, g.ny, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune);
+    if (nyw <= 0) { ybase = 1; nyw = g.ny; }
+    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune);
     p.sm.rev = seg_rev(a->tune);
+    p.sm.ybase = ybase;
     dim3 grd(p.nbands, p.nseg);
     SegMap sm = p.sm;
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
@@ -368,16 +372,16 @@ int pick_warps(const fkc_grid& g, bool fast, int red, const fkc_sw_tune& t) {
 }
 
 template <class T, bool FAST, int RED>
-int launch_tma_nw(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m) {
+int launch_tma_nw(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* m, int ybase, int nyw) {
     switch (pick_warps<T>(a->grid, FAST, RED, a->tune)) {
-        case 1: return launch_tma_t<T, FAST, RED, 1>(a, st, m);
-        case 2: return launch_tma_t<T, FAST, RED, 2>(a, st, m);
-        default: return launch_tma_t<T, FAST, RED, 4>(a, st, m);
+        case 1: return launch_tma_t<T, FAST, RED, 1>(a, st, m, ybase, nyw);
+        case 2: return launch_tma_t<T, FAST, RED, 2>(a, st, m, ybase, nyw);
+        default: return launch_tma_t<T, FAST, RED, 4>(a, st, m, ybase, nyw);
     }
 }
 
 template <class T>
-int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
+int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st, int ybase, int nyw) {
     CUtensorMap m[3];  // H, U, V
     const fkc_grid& g = a->grid;
     const void* ps[3] = {a->H, a->U, a->V};
@@ -389,15 +393,16 @@ int launch_tma_typed(const fkc_sw_step_args* a, cudaStream_t st) {
     const RedPtrs rp = to_red(a->red);
     const int lvl = rp.cfl_min ? 2 : (any_red(rp) ? 1 : 0);
     if (fast) {
-        if (lvl == 2) return launch_tma_nw<T, true, 2>(a, st, m);
-        return lvl ? launch_tma_nw<T, true, 1>(a, st, m) : launch_tma_nw<T, true, 0>(a, st, m);
+        if (lvl == 2) return launch_tma_nw<T, true, 2>(a, st, m, ybase, nyw);
+        return lvl ? launch_tma_nw<T, true, 1>(a, st, m, ybase, nyw) : launch_tma_nw<T, true, 0>(a, st, m, ybase, nyw);
     }
-    if (lvl == 2) return launch_tma_nw<T, false, 2>(a, st, m);
-    return lvl ? launch_tma_nw<T, false, 1>(a, st, m) : launch_tma_nw<T, false, 0>(a, st, m);
+    if (lvl == 2) return launch_tma_nw<T, false, 2>(a, st, m, ybase, nyw);
+    return lvl ? launch_tma_nw<T, false, 1>(a, st, m, ybase, nyw) : launch_tma_nw<T, false, 0>(a, st, m, ybase, nyw);
 }
 
-int launch_tma(const fkc_sw_step_args* a, cudaStream_t st) {
-    return a->grid.dtype == FKC_F32 ? launch_tma_typed<float>(a, st) : launch_tma_typed<double>(a, st);
+int launch_tma(const fkc_sw_step_args* a, cudaStream_t st, int ybase = 1, int nyw = 0) {
+    return a->grid.dtype == FKC_F32 ? launch_tma_typed<float>(a, st, ybase, nyw)
+                                    : launch_tma_typed<double>(a, st, ybase, nyw);
 }
 
 // ---------------------------------------------------------------------------
@@ -627,7 +632,7 @@ int launch_loop_t(const fkc_sw_loop_args* L, cudaStream_t st, bool forced) {
     ctl.per_du = s.bc[2] == FKC_BC_PERIODIC;
     ctl.dt = s.dt;
     ctl.cfl = s.cfl;
-    SegMap sm{seg, 0, 0, 0};
+    SegMap sm{seg, 0, 0, 0, 1, g.ny};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nbands, nseg);
     cfg.blockDim = dim3(B::THREADS);
@@ -867,6 +872,414 @@ int fkc_sw_advance_n(const fkc_sw_loop_args* L, void* stream) {
     err = cudaGraphLaunch(exec, st);
     if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(err));
     return FKC_OK;
+}
+
+extern "C++" {
+// one wavefront launch (sw_wave_tma): tasks of one band and step each
+template <class T, bool FAST, int RED, int NW>
+int launch_wave_t(const fkc_sw_step_args* a, const WaveArgs& w, int band_rows, cudaStream_t st) {
+    using G = tma::Geo<T>;
+    using B = tma::Blk<T, NW>;
+    auto kern = sw_wave_tma<T, FAST, RED, NW>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM_BYTES);
+    });
+    if (attr_err != cudaSuccess) return fail(FKC_ECUDA, "wave kernel attributes: %s", cudaGetErrorString(attr_err));
+    const fkc_grid& g = a->grid;
+    CUtensorMap m[6];
+    const void* ps[6] = {a->H, a->U, a->V, a->oH, a->oU, a->oV};
+    for (int f = 0; f < 6; ++f)
+        if (int rc = get_map(ps[f], g.nx, g.ny, g.pitch, G::BOXW, (int)sizeof(T), &m[f])) return rc;
+    const int nstrips = (g.nx + G::OWN - 1) / G::OWN;
+    const int nbands = (nstrips + NW - 1) / NW;
+    dim3 grd(nbands, (band_rows + w.seg - 1) / w.seg, w.ntask);
+    LoopBufs bufs{{(void*)a->H, (void*)a->U, (void*)a->V}, {a->oH, a->oU, a->oV}};
+    launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, !a->tune.no_pdl, m[0], m[1], m[2], m[3], m[4], m[5],
+                g.nx, g.ny, g.pitch, a->tune.no_alternate ? 0 : 1, bufs, (T)a->dx, (T)a->dy, (T)a->dt, (T)a->g,
+                to_bcs(a->bc), w);
+    return check_launch("sw_wave_tma");
+}
+
+// the wave kernel's schedule: warps per CTA and rows per segment for a launch
+// of ntask bands of band_rows rows (a grid of nx x ntask*band_rows cells)
+template <class T>
+void wave_plan(const fkc_sw_step_args* a, int band_rows, int ntask, bool fast, int red, int& nw, int& seg) {
+    fkc_grid eq = a->grid;
+    eq.ny = band_rows * ntask;
+    nw = pick_warps<T>(eq, fast, red, a->tune);
+    const int wps = sizeof(T) == 8 ? tma::Geo<T>::template warps_per_sm<true, 0>()
+                                   : (fast ? tma::Geo<T>::template warps_per_sm<true, 0>()
+                                           : tma::Geo<T>::template warps_per_sm<false, 0>());
+    const int nstrips = (a->grid.nx + tma::Geo<T>::OWN - 1) / tma::Geo<T>::OWN;
+    fkc_sw_tune t = a->tune;
+    seg = pick_seg((nstrips + nw - 1) / nw * ntask, band_rows, wps / nw, t);
+}
+
+template <class T>
+int launch_wave(const fkc_sw_step_args* a, const WaveArgs& w0, int band_rows, cudaStream_t st) {
+    const bool fast = a->mode == FKC_MODE_FAST;
+    const int red = w0.t[0].red_row ? 1 : 0;
+    int nw, seg;
+    wave_plan<T>(a, band_rows, w0.ntask, fast, red, nw, seg);
+    WaveArgs w = w0;
+    w.seg = seg;
+#define WAVE_NW(F, R) \
+    (nw == 1 ? launch_wave_t<T, F, R, 1>(a, w, band_rows, st) \
+             : nw == 2 ? launch_wave_t<T, F, R, 2>(a, w, band_rows, st) : launch_wave_t<T, F, R, 4>(a, w, band_rows, st))
+    if (fast) return red ? WAVE_NW(true, 1) : WAVE_NW(true, 0);
+    return red ? WAVE_NW(false, 1) : WAVE_NW(false, 0);
+#undef WAVE_NW
+}
+
+}  // extern "C++"
+
+// ---------------------------------------------------------------------------
+// streamed host run (fkc_sw_run_host): upload, steps and download overlapped
+// ---------------------------------------------------------------------------
+int fkc_sw_reduce_state(const fkc_grid* g, const void* H, const void* U, const void* V, double dx, double dy,
+                        double gravity, const fkc_sw_reduce* red, void* stream);
+int fkc_region_cpy(int32_t dtype, const void* src, int32_t nx_full, int32_t ny_full, int64_t src_pitch,
+                   const int32_t halo[4], void* dst, int64_t dst_pitch, void* stream);
+namespace {
+// step args of global step i (buffers by parity, reduction row i+1)
+fkc_sw_step_args step_of(const fkc_sw_loop_args* L, int64_t i) {
+    fkc_sw_step_args a = L->step;
+    const bool even = (i & 1) == 0;
+    a.H = even ? L->step.H : L->step.oH;
+    a.U = even ? L->step.U : L->step.oU;
+    a.V = even ? L->step.V : L->step.oV;
+    a.oH = even ? L->step.oH : (void*)L->step.H;
+    a.oU = even ? L->step.oU : (void*)L->step.U;
+    a.oV = even ? L->step.oV : (void*)L->step.V;
+    if (L->slots) {
+        uint64_t* out = L->slots + 5 * (i + 1);
+        a.red.mass = (double*)out;
+        a.red.max_abs_u = out + 1;
+        a.red.max_abs_v = out + 2;
+        a.red.cfl_min = L->want_cfl ? out + 3 : nullptr;
+        a.red.err = (uint32_t*)(out + 4);
+    }
+    a.dt_bound = nullptr;
+    a.tune.parity = (int32_t)(i & 1);
+    return a;
+}
+
+struct CopyStreams {
+    cudaStream_t up = nullptr, down = nullptr, red = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t last = nullptr;      // end of the previous call (calls share the streams and the staging)
+    char* stage = nullptr;           // staging slots, grow-only
+    size_t stage_bytes = 0;
+};
+std::mutex g_cs_mu;
+CopyStreams g_cs[64];
+
+int copy_streams(CopyStreams** out, size_t nev) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(FKC_ECUDA, "cudaGetDevice");
+    CopyStreams& c = g_cs[dev];
+    if (!c.up) {
+        if (cudaStreamCreateWithFlags(&c.up, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c.down, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c.red, cudaStreamNonBlocking) != cudaSuccess)
+            return fail(FKC_ECUDA, "cudaStreamCreate (copy streams)");
+    }
+    if (!c.last && cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming) != cudaSuccess)
+        return fail(FKC_ECUDA, "cudaEventCreate");
+    while (c.ev.size() < nev) {
+        cudaEvent_t e;
+        // timing-enabled under FKC_STREAM_TRACE (the trace below reads them)
+        const unsigned fl = getenv("FKC_STREAM_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+        if (cudaEventCreateWithFlags(&e, fl) != cudaSuccess) return fail(FKC_ECUDA, "cudaEventCreate");
+        c.ev.push_back(e);
+    }
+    *out = &c;
+    return FKC_OK;
+}
+}  // namespace
+
+int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], void* const host_out[3],
+                    int64_t host_pitch_bytes, int32_t band_rows, void* stream) {
+    if (!L || !host_in || !host_out) return fail(FKC_EUSAGE, "null args");
+    const fkc_sw_step_args& s0 = L->step;
+    const fkc_grid& g = s0.grid;
+    if (!valid_grid(&g)) return fail(FKC_EUSAGE, "invalid grid");
+    for (int f = 0; f < 3; ++f)
+        if (!host_in[f] || !host_out[f]) return fail(FKC_EUSAGE, "null host field");
+    const int es = g.dtype == FKC_F32 ? 4 : 8;
+    if (host_pitch_bytes < (int64_t)(g.nx + 2) * es || host_pitch_bytes % es)
+        return fail(FKC_EUSAGE, "host pitch below a full row or not a multiple of the element size");
+    if (L->steps < 0 || L->first_step < 0 || band_rows < 0) return fail(FKC_EUSAGE, "negative steps / band_rows");
+    if (L->dt_from_slots) return fail(FKC_EUSAGE, "fkc_sw_run_host: fixed dt only (a CFL dt needs every band of a step)");
+    if (s0.bc[2] == FKC_BC_PERIODIC) return fail(FKC_EUSAGE, "fkc_sw_run_host: periodic rows wrap around the wavefront");
+    if (s0.sync.counter || s0.peer[0].p[0] || s0.peer[1].p[0] || s0.peer[2].p[0] || s0.peer[3].p[0])
+        return fail(FKC_EUSAGE, "fkc_sw_run_host: no peer lines");
+    if (!tma_eligible(&s0)) return fail(FKC_EUSAGE, "fkc_sw_run_host: needs the TMA layout (nx, pitch, alignment)");
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lk(g_cs_mu);     // the copy streams and events are per device, shared
+    // bands of ~band_rows interior rows (auto: 128 bands, >= 16 rows): the
+    // wavefront's lag is 2 bands per step, each launch carries a fixed cost
+    // (B200, 16384^2 x 20 steps, profiles/r02/stream_timing.txt: 64 rows
+    // 120 ms, 96 / 128 rows 98 / 99 ms, 256 rows 108 ms, 384 rows 121 ms)
+    int br = band_rows > 0 ? band_rows : (g.ny + 127) / 128;
+    if (br < 16) br = 16;
+    if (br > g.ny) br = g.ny;
+    const int nb = (g.ny + br - 1) / br;
+    CopyStreams* cs = nullptr;
+    if (int rc = copy_streams(&cs, (size_t)5 * nb + 2)) return rc;
+    cudaEvent_t* ev_up = cs->ev.data();            // [nb]   chunk i in its upload staging slot
+    cudaEvent_t* ev_rep = cs->ev.data() + nb;      // [nb]   chunk i unpacked into the field (slot free)
+    cudaEvent_t* ev_done = cs->ev.data() + 2 * nb; // [nb]   band i final, packed into its download slot
+    cudaEvent_t* ev_dl = cs->ev.data() + 3 * nb;   // [nb]   band i downloaded (slot free)
+    cudaEvent_t* ev_red = cs->ev.data() + 4 * nb;  // [nb]   band i of the uploaded state reduced
+    cudaEvent_t ev_start = cs->ev[5 * nb], ev_end = cs->ev[5 * nb + 1];
+    const int64_t S = L->steps, f0 = L->first_step;
+    const int64_t dpitch = g.pitch * es, row_b = (int64_t)(g.nx + 2) * es;
+    const bool in_a = (f0 & 1) == 0, out_a = ((f0 + S) & 1) == 0;
+    const void* A[3] = {s0.H, s0.U, s0.V};
+    const void* Bf[3] = {s0.oH, s0.oU, s0.oV};
+    // full rows of chunk i: [r_lo, r_hi] (the halo rows travel with the first / last band)
+    auto chunk = [&](int i, int& r_lo, int& r_hi) {
+        r_lo = i == 0 ? 0 : 1 + i * br;
+        r_hi = i == nb - 1 ? g.ny + 1 : (i + 1) * br;
+    };
+    auto band = [&](int i, int& lo, int& n) {
+        lo = 1 + i * br;
+        n = (i == nb - 1 ? g.ny : (i + 1) * br) - lo + 1;
+    };
+    cudaError_t e;
+    // The copies are 1-D (the host rows of a chunk are one contiguous block):
+    // PCIe runs both directions at full rate only for linear copies (B200:
+    // 55 + 55 GB/s at once vs 74 GB/s in total for pitched 2-D ones).  A
+    // chunk lands in a device staging slot with the host row pitch and is
+    // unpacked into the padded field by a copy kernel (and the other way
+    // round for downloads); NS slots per direction, reused behind events.
+    constexpr int NS = 16;
+    const int64_t hp_el = host_pitch_bytes / es;
+    const int64_t slot_field = (int64_t)(br + 2) * host_pitch_bytes;
+    const int64_t slot_bytes = 3 * slot_field;
+    // the previous call may still use the staging slots
+    cudaStreamWaitEvent(st, cs->last, 0);
+    if (cs->stage_bytes < (size_t)(2 * NS * slot_bytes)) {
+        if (cs->stage) {
+            cudaDeviceSynchronize();
+            cudaFree(cs->stage);
+            cs->stage = nullptr;
+            cs->stage_bytes = 0;
+        }
+        e = cudaMalloc((void**)&cs->stage, (size_t)(2 * NS * slot_bytes));
+        if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMalloc (staging, %lld bytes): %s",
+                                          (long long)(2 * NS * slot_bytes), cudaGetErrorString(e));
+        cs->stage_bytes = (size_t)(2 * NS * slot_bytes);
+    }
+    char* stage = cs->stage;
+    char* stage_up = stage;
+    char* stage_dn = stage + NS * slot_bytes;
+    const int32_t no_halo[4] = {0, 0, 0, 0};
+    auto host_block = [&](int r_lo, int r_hi) { return (int64_t)(r_hi - r_lo) * host_pitch_bytes + row_b; };
+    // upload chunk i: H2D into slot i % NS (after the slot's previous chunk was
+    // unpacked), then unpack it into the input buffer on the compute stream
+    auto upload_ = [&](int i) -> int {
+        int r_lo, r_hi;
+        chunk(i, r_lo, r_hi);
+        char* slot = stage_up + (int64_t)(i % NS) * slot_bytes;
+        if (i >= NS) cudaStreamWaitEvent(cs->up, ev_rep[i - NS], 0);
+        for (int f = 0; f < 3; ++f) {
+            e = cudaMemcpyAsync(slot + f * slot_field, (const char*)host_in[f] + (int64_t)r_lo * host_pitch_bytes,
+                                (size_t)host_block(r_lo, r_hi), cudaMemcpyHostToDevice, cs->up);
+            if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (upload %d): %s", i, cudaGetErrorString(e));
+        }
+        cudaEventRecord(ev_up[i], cs->up);
+        cudaStreamWaitEvent(st, ev_up[i], 0);
+        for (int f = 0; f < 3; ++f) {
+            char* dev = (char*)(in_a ? A[f] : Bf[f]) + (int64_t)r_lo * dpitch;
+            if (int rc = fkc_region_cpy(g.dtype, slot + f * slot_field, g.nx + 2, r_hi - r_lo + 1, hp_el, no_halo, dev,
+                                        g.pitch, st))
+                return rc;
+        }
+        cudaEventRecord(ev_rep[i], st);
+        return FKC_OK;
+    };
+    // download band i (its final state, compute-stream order): pack into slot
+    // i % NS (after the slot's previous band left), then D2H
+    auto download_ = [&](int i) -> int {
+        int r_lo, r_hi;
+        chunk(i, r_lo, r_hi);
+        char* slot = stage_dn + (int64_t)(i % NS) * slot_bytes;
+        if (i >= NS) cudaStreamWaitEvent(st, ev_dl[i - NS], 0);
+        for (int f = 0; f < 3; ++f) {
+            const char* dev = (const char*)(out_a ? A[f] : Bf[f]) + (int64_t)r_lo * dpitch;
+            if (int rc = fkc_region_cpy(g.dtype, dev, g.nx + 2, r_hi - r_lo + 1, g.pitch, no_halo, slot + f * slot_field,
+                                        hp_el, st))
+                return rc;
+        }
+        cudaEventRecord(ev_done[i], st);
+        cudaStreamWaitEvent(cs->down, ev_done[i], 0);
+        for (int f = 0; f < 3; ++f) {
+            e = cudaMemcpyAsync((char*)host_out[f] + (int64_t)r_lo * host_pitch_bytes, slot + f * slot_field,
+                                (size_t)host_block(r_lo, r_hi), cudaMemcpyDeviceToHost, cs->down);
+            if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (download %d): %s", i, cudaGetErrorString(e));
+        }
+        cudaEventRecord(ev_dl[i], cs->down);
+        return FKC_OK;
+    };
+    auto row_back = [&](int64_t sidx) -> int {
+        if (!L->slots || !L->host_slots) return FKC_OK;
+        const int64_t r = f0 + sidx + 1;
+        e = cudaMemcpyAsync(L->host_slots + 5 * r, L->slots + 5 * r, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+        return e == cudaSuccess ? FKC_OK : fail(FKC_ECUDA, "cudaMemcpyAsync (diagnostics row): %s", cudaGetErrorString(e));
+    };
+    // diagnostics row of the uploaded state (row first_step), band by band as
+    // the bands arrive, on a side stream (the step that overwrites band i of
+    // the input buffer -- the run's second -- waits for it)
+    auto reduce_initial = [&](int i) -> int {
+        if (!L->slots) return FKC_OK;
+        cudaStreamWaitEvent(cs->red, ev_rep[i], 0);
+        int lo, n;
+        band(i, lo, n);
+        fkc_grid sub = g;
+        sub.ny = n;
+        const int64_t off = (int64_t)(lo - 1) * dpitch;
+        fkc_sw_reduce red{};
+        uint64_t* row = L->slots + 5 * f0;
+        red.mass = (double*)row;
+        red.max_abs_u = row + 1;
+        red.max_abs_v = row + 2;
+        red.cfl_min = row + 3;
+        red.err = (uint32_t*)(row + 4);
+        const char* base[3] = {(const char*)(in_a ? A[0] : Bf[0]), (const char*)(in_a ? A[1] : Bf[1]),
+                               (const char*)(in_a ? A[2] : Bf[2])};
+        if (int rc = fkc_sw_reduce_state(&sub, base[0] + off, base[1] + off, base[2] + off, s0.dx, s0.dy, s0.g, &red,
+                                         cs->red))
+            return rc;
+        cudaEventRecord(ev_red[i], cs->red);
+        return FKC_OK;
+    };
+    // the copy streams start after the caller's prior work
+    cudaEventRecord(ev_start, st);
+    cudaStreamWaitEvent(cs->up, ev_start, 0);
+    cudaStreamWaitEvent(cs->down, ev_start, 0);
+    cudaStreamWaitEvent(cs->red, ev_start, 0);
+    // Phases: (1) the first P steps band by band as a wavefront behind the
+    // upload (step s of band i after step s-1 of bands i-1 .. i+1 -- which also
+    // covers the double buffer's write-after-read -- and after the upload of
+    // band i+1); (2) whole-grid steps;
+    // (3) the last P steps as a wavefront, each band downloaded as soon as
+    // its last step is done.  With S <= 2P there is no phase 2.
+    const int64_t P = 32;
+    const int64_t s1 = S < P ? S : P;                        // steps of phase 1
+    const int64_t s3 = (S - s1) < P ? (S - s1) : P;          // steps of phase 3
+    const int64_t s2 = S - s1 - s3;
+    // Iteration t launches ONE wave kernel with the tasks (step sa+k, band
+    // t-2k-lag), k = 0 .. : step s of band i follows step s-1 of bands
+    // i-1 .. i+1 (earlier iterations) -- which also covers the double
+    // buffer's write-after-read -- and the upload of band i+lag; tasks of
+    // one launch are two bands apart, so none reads rows another writes.
+    const bool trace = getenv("FKC_STREAM_TRACE") != nullptr;
+    std::vector<cudaEvent_t> trace_ev;               // [launch start, launch end] pairs (trace mode)
+    fkc_sw_step_args a0 = s0;                       // H,U,V = buffer A, oH,oU,oV = buffer B
+    a0.red = fkc_sw_reduce{};                       // per task (WaveTask::red_row)
+    a0.dt_bound = nullptr;
+    auto wavefront = [&](int64_t sa, int64_t sb, bool upload, bool download) -> int {
+        const int lag = upload ? 1 : 0;
+        const int64_t tmax = (int64_t)nb + 2 * (sb - sa) + 2;
+        for (int64_t t = 0; t < tmax; ++t) {
+            if (upload && t < nb) {
+                if (int rc = upload_((int)t)) return rc;
+                if (int rc = reduce_initial((int)t)) return rc;
+            }
+            WaveArgs w{};
+            int64_t last_of[WAVE_MAX_TASKS];
+            for (int64_t sidx = sa; sidx < sb && w.ntask < WAVE_MAX_TASKS; ++sidx) {
+                const int64_t i = t - 2 * (sidx - sa) - lag;
+                if (i < 0 || i >= nb) continue;
+                int lo, n;
+                band((int)i, lo, n);
+                const int64_t gi = f0 + sidx;
+                WaveTask& tk = w.t[w.ntask];
+                tk.odd = (int)(gi & 1);
+                tk.ybase = lo;
+                tk.nyw = n;
+                tk.red_row = L->slots ? (unsigned long long*)(L->slots + 5 * (gi + 1)) : nullptr;
+                last_of[w.ntask] = (i == nb - 1) ? sidx : -1;
+                ++w.ntask;
+                if (sidx == 1 && L->slots) cudaStreamWaitEvent(st, ev_red[i], 0);   // overwrites band i of the input
+            }
+            if (w.ntask == 0) continue;
+            if (trace) {
+                cudaEvent_t e0;
+                cudaEventCreate(&e0);
+                cudaEventRecord(e0, st);
+                trace_ev.push_back(e0);
+            }
+            const int rc = g.dtype == FKC_F32 ? launch_wave<float>(&a0, w, br, st) : launch_wave<double>(&a0, w, br, st);
+            if (rc) return rc;
+            if (trace) {
+                cudaEvent_t e1;
+                cudaEventCreate(&e1);
+                cudaEventRecord(e1, st);
+                trace_ev.push_back(e1);
+            }
+            for (int k = 0; k < w.ntask; ++k)
+                if (last_of[k] >= 0)
+                    if (int rc2 = row_back(last_of[k])) return rc2;
+            if (download) {
+                // the band whose last step ran in this launch: i = t - 2(sb-1-sa) - lag
+                const int64_t i = t - 2 * (sb - 1 - sa) - lag;
+                if (i >= 0 && i < nb)
+                    if (int rc2 = download_((int)i)) return rc2;
+            }
+        }
+        return FKC_OK;
+    };
+    if (S == 0) {
+        for (int i = 0; i < nb; ++i) {
+            if (int rc = upload_(i)) return rc;
+            if (int rc = reduce_initial(i)) return rc;
+            if (int rc = download_(i)) return rc;
+        }
+    } else {
+        if (int rc = wavefront(0, s1, true, s2 == 0 && s3 == 0)) return rc;
+        for (int64_t sidx = s1; sidx < s1 + s2; ++sidx) {
+            fkc_sw_step_args a = step_of(L, f0 + sidx);
+            if (int rc = launch_tma(&a, st)) return rc;
+            if (int rc = row_back(sidx)) return rc;
+        }
+        if (s3 > 0)
+            if (int rc = wavefront(s1 + s2, S, false, true)) return rc;
+    }
+    // the caller's stream continues after the last download and reduction
+    cudaEventRecord(ev_end, cs->red);
+    cudaStreamWaitEvent(st, ev_end, 0);
+    cudaEventRecord(ev_end, cs->down);
+    cudaStreamWaitEvent(st, ev_end, 0);
+    cudaEventRecord(cs->last, st);
+    if (getenv("FKC_STREAM_TRACE")) {
+        // diagnostics: when each band's upload and last step completed (ms
+        // after the start), and the end -- synchronises the device
+        cudaEventSynchronize(ev_end);
+        float te = 0.f;
+        cudaEventElapsedTime(&te, ev_start, ev_end);
+        fprintf(stderr, "fkc_sw_run_host trace: %d bands of %d rows, %lld steps, end %.3f ms\n", nb, br, (long long)S, te);
+        for (int i = 0; i < nb; i += (nb > 16 ? nb / 16 : 1)) {
+            float tu = -1.f, td = -1.f;
+            if (S > 0 && cudaEventQuery(ev_up[i]) == cudaSuccess) cudaEventElapsedTime(&tu, ev_start, ev_up[i]);
+            if (S > 0 && cudaEventQuery(ev_done[i]) == cudaSuccess) cudaEventElapsedTime(&td, ev_start, ev_done[i]);
+            fprintf(stderr, "  band %4d: uploaded %8.3f ms, last step done %8.3f ms\n", i, tu, td);
+        }
+        cudaDeviceSynchronize();
+        for (size_t k = 0; k + 1 < trace_ev.size(); k += 2) {
+            if (k / 2 % 16 != 0) continue;
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, ev_start, trace_ev[k]);
+            cudaEventElapsedTime(&b, trace_ev[k], trace_ev[k + 1]);
+            fprintf(stderr, "  wave launch %4zu: starts %8.3f ms, runs %7.3f ms\n", k / 2, a, b);
+        }
+        for (auto e : trace_ev) cudaEventDestroy(e);
+    }
+    return check_launch("fkc_sw_run_host");
 }
 
 int fkc_sw_apply_boundary(const fkc_grid* g, void* H, void* U, void* V, const int32_t bc[4], void* stream) {

@@ -254,13 +254,17 @@ __device__ __forceinline__ void issue_stage(uint32_t st, uint32_t bar, const CUt
 // starts where the previous one ended: its first CTAs read rows the previous
 // step wrote last, which are still in L2 (the host alternates `rev` per
 // launch on a stream).
+// The segments tile the row window [ybase, ybase + nyw) -- the whole
+// interior (ybase 1, nyw = ny) for a time step, a band of it for the
+// streamed host run (fkc_sw_run_host), whose bands advance as a wavefront.
 struct SegMap {
     int seg, tail, jt, rev;
+    int ybase, nyw;
 };
-__device__ __forceinline__ void seg_rows(const SegMap& m, int j, int ny, int& y0, int& nrows) {
+__device__ __forceinline__ void seg_rows(const SegMap& m, int j, int& y0, int& nrows) {
     const int r0 = (m.tail == 0 || j < m.jt) ? j * m.seg : m.jt * m.seg + (j - m.jt) * m.tail;
-    nrows = min((m.tail == 0 || j < m.jt) ? m.seg : m.tail, ny - r0);
-    y0 = m.rev ? ny + 1 - r0 - nrows : 1 + r0;     // rows y0 .. y0 + nrows - 1
+    nrows = min((m.tail == 0 || j < m.jt) ? m.seg : m.tail, m.nyw - r0);
+    y0 = m.rev ? m.ybase + m.nyw - r0 - nrows : m.ybase + r0;     // rows y0 .. y0 + nrows - 1
 }
 
 template <class T, int CPL> struct Row3 {
@@ -406,7 +410,7 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
     const int tx = G::VEC == 16 ? txl : (txl & ~1);      // box start (16-B aligned)
     if (xs + CPL > nx) return 0;                         // strip owns nothing (ragged last band)
     int y0, nrows;                                       // first interior row of the segment, rows
-    seg_rows(sm, blockIdx.y, ny, y0, nrows);
+    seg_rows(sm, blockIdx.y, y0, nrows);
     const int nload = nrows + 2;                         // rows y0-1 .. y0+nrows
     const int nstages = (nload + R - 1) / R;
     // Sweep direction (fast mode): with `alt`, odd segments sweep top-down,
@@ -517,7 +521,7 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         uint32_t cy;
         asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(cy));
         int yy0, nr;
-        seg_rows(sm, (int)cy, ny, yy0, nr);
+        seg_rows(sm, (int)cy, yy0, nr);
         return k < (nr + 2 + R - 1) / R;
     };
     for (int k = 0; stages_left(k); ++k) {
@@ -690,6 +694,57 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
     __syncwarp();                                 // the barriers are initialised before any lane uses them
     pdl_wait();                                   // the previous step's output is complete
     tma_sweep<T, FAST, RED, NW>(&tmH, &tmU, &tmV, nx, ny, pitch, sm, alt, oH, oU, oV, dx, dy, dts, g, bc, red, P, sy,
+                                sbase, 0u);
+}
+
+// ---------------------------------------------------------------------------
+// Wavefront launch of the streamed host run (fkc_sw_run_host): one launch
+// advances several row bands, each by one step of its own (task k =
+// blockIdx.z: band rows [ybase, ybase + nyw), global step parity -> which
+// buffer it reads / writes, its step's reduction row).  The host schedules
+// tasks of one launch two bands apart per step, so no task reads rows
+// another task of the same launch writes.
+// ---------------------------------------------------------------------------
+constexpr int WAVE_MAX_TASKS = 40;
+struct WaveTask {
+    int odd;                       // global step parity: 0 reads A writes B, 1 reads B writes A
+    int ybase, nyw;
+    unsigned long long* red_row;   // 5-word reduction row of the task's step, or null
+};
+struct WaveArgs {
+    WaveTask t[WAVE_MAX_TASKS];
+    int ntask, seg;
+};
+
+template <class T, bool FAST, int RED, int NW>
+__global__ void __launch_bounds__(NW * 32, tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>())
+sw_wave_tma(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+            const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mB0,
+            const __grid_constant__ CUtensorMap mB1, const __grid_constant__ CUtensorMap mB2, int nx, int ny,
+            int64_t pitch, int alt, const __grid_constant__ LoopBufs bufs, T dx, T dy, T dt, T g,
+            const __grid_constant__ BCs bc, const __grid_constant__ WaveArgs w) {
+    const WaveTask& tk = w.t[blockIdx.z];
+    pdl_launch_dependents();
+    if ((int)blockIdx.y * w.seg >= tk.nyw) return;           // this task has fewer segments
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const SegMap sm{w.seg, 0, 0, 0, tk.ybase, tk.nyw};
+    const bool odd = tk.odd != 0;
+    void* const* out = odd ? bufs.a : bufs.b;
+    RedPtrs red{nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (tk.red_row)
+        red = RedPtrs{(double*)tk.red_row, tk.red_row + 1, tk.red_row + 2, nullptr, (uint32_t*)(tk.red_row + 4)};
+    const DtSrc dts{(double)dt, nullptr, 1.0};
+    pdl_wait();                                   // the previous launch's output is complete
+    tma_sweep<T, FAST, RED, NW>(odd ? &mB0 : &mA0, odd ? &mB1 : &mA1, odd ? &mB2 : &mA2, nx, ny, pitch, sm, alt,
+                                (T*)out[0], (T*)out[1], (T*)out[2], dx, dy, dts, g, bc, red, c_no_peers, c_no_sync,
                                 sbase, 0u);
 }
 

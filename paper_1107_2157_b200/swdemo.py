@@ -490,28 +490,93 @@ class Simulation:
         return ReductionSlots.decode(self.slots.buf[: self.n + 1].cpu().numpy())
 
     def rows(self) -> RunResult:
-        d = self.diagnostics()
-        cfg = self.cfg
-        f = dtype_of(cfg.precision).type
-        rows = []
-        dts = []
-        t = self.t0
         # the steps run with the state's own spacing (SWState.dx / dy), so the
         # mass does too
-        cell_area = self.a.dx * self.a.dy
-        if d["err"][0]:
-            raise_for_error(int(d["err"][0]), "in the initial state")
-        for k in range(self.n):
-            if d["err"][k + 1]:
-                raise_for_error(int(d["err"][k + 1]), f"at step {k + 1}")
-            dt = float(cfg.dt) if cfg.dt is not None else float(f(cfg.cfl_factor) * f(d["cfl_min"][k]))
-            t += dt
-            dts.append(dt)
-            rows.append((k + 1, t, dt, float(d["mass"][k + 1]) * cell_area,
-                         float(d["max_hu"][k + 1]), float(d["max_hv"][k + 1])))
-        st = self.state()
-        st.t = t
-        return RunResult(rows, st, np.array(dts))
+        return _run_result(self.cfg, self.diagnostics(), self.n, self.t0, self.a.dx * self.a.dy, self.state())
+
+
+def _run_result(cfg: SWConfig, d: dict, n: int, t0: float, cell_area: float, st: SWState) -> RunResult:
+    """The per-step rows (step, t, dt, mass, max|hu|, max|hv|) of a run from
+    its decoded reduction rows; raises the SPEC errors a row reports."""
+    f = dtype_of(cfg.precision).type
+    rows = []
+    dts = []
+    t = t0
+    if d["err"][0]:
+        raise_for_error(int(d["err"][0]), "in the initial state")
+    for k in range(n):
+        if d["err"][k + 1]:
+            raise_for_error(int(d["err"][k + 1]), f"at step {k + 1}")
+        dt = float(cfg.dt) if cfg.dt is not None else float(f(cfg.cfl_factor) * f(d["cfl_min"][k]))
+        t += dt
+        dts.append(dt)
+        rows.append((k + 1, t, dt, float(d["mass"][k + 1]) * cell_area,
+                     float(d["max_hu"][k + 1]), float(d["max_hv"][k + 1])))
+    st.t = t
+    return RunResult(rows, st, np.array(dts))
+
+
+# grids from this size up take the streamed host path (below it a run is
+# short next to its copies' latency, and the resident / per-step paths apply)
+STREAM_MIN_CELLS = 1 << 20
+
+
+def _host_arrays(st: SWState):
+    return [getattr(st, n).data for n in ("H", "U", "V")]
+
+
+def _streamable(cfg: SWConfig, state: SWState, out: Optional[SWState]) -> bool:
+    """fkc_sw_run_host's domain: fixed dt, no periodic rows, the TMA layout,
+    C-contiguous host arrays of one row pitch (in and out)."""
+    if cfg.dt is None or state.on_device:
+        return False
+    bc = _bc4(cfg.boundary)
+    if bc[2] == N.BC_PERIODIC or cfg.variant not in ("auto", "tma"):
+        return False
+    nx, ny = state.full.nx - 2, state.full.ny - 2
+    cpl = 4 if state.precision == "f32" else 2
+    if nx % cpl or nx * ny < STREAM_MIN_CELLS:
+        return False
+    arrs = _host_arrays(state) + (_host_arrays(out) if out is not None else [])
+    for a in arrs:
+        if not isinstance(a, np.ndarray) or not a.flags.c_contiguous or a.dtype != dtype_of(state.precision) \
+                or a.shape != (ny + 2, nx + 2):
+            return False
+    return True
+
+
+def _run_streamed(cfg: SWConfig, state: SWState, out: Optional[SWState], tune: Optional[N.Tune] = None,
+                  band_rows: int = 0) -> RunResult:
+    """run() from and to host memory with the copies overlapping the steps
+    (fkc_sw_run_host): the bands of the state are stepped while later ones
+    are still uploading and downloaded as soon as their last step is done."""
+    torch = _torch()
+    full, prec = state.full, state.precision
+    a = SWState(DeviceField(full, prec), DeviceField(full, prec), DeviceField(full, prec),
+                state.g, state.dx, state.dy, state.t)
+    b = SWState(a.H.empty_like(), a.U.empty_like(), a.V.empty_like(), state.g, state.dx, state.dy, state.t)
+    if out is None:
+        out = SWState(*(Field(full, np.empty((full.ny, full.nx), dtype_of(prec)), prec) for _ in range(3)),
+                      state.g, state.dx, state.dy, state.t)
+    slots = ReductionSlots(cfg.steps + 1, a.H.storage.device)
+    host_rows = torch.zeros((cfg.steps + 1, 5), dtype=torch.int64, pin_memory=True)
+    L = N.LoopArgs()
+    L.step = _step_args(a, b, cfg.dt, cfg.boundary, cfg.mode, cfg.variant, None, None, cfg.cfl_factor, tune)
+    L.first_step = 0
+    L.steps = cfg.steps
+    L.slots = slots.buf.data_ptr()
+    L.host_slots = host_rows.data_ptr()
+    src = (ctypes.c_void_p * 3)(*(x.ctypes.data for x in _host_arrays(state)))
+    dst = (ctypes.c_void_p * 3)(*(x.ctypes.data for x in _host_arrays(out)))
+    stream = torch.cuda.current_stream()
+    N.check(N.lib().fkc_sw_run_host(ctypes.byref(L), src, dst, _host_arrays(state)[0].strides[0], band_rows,
+                                    stream.cuda_stream))
+    stream.synchronize()
+    # row 0 (the uploaded state) was reduced band by band inside the call
+    host_rows[0].copy_(slots.buf[0])
+    d = ReductionSlots.decode(host_rows.numpy())
+    out.g, out.dx, out.dy = state.g, state.dx, state.dy
+    return _run_result(cfg, d, cfg.steps, state.t, state.dx * state.dy, out)
 
 
 def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
@@ -524,11 +589,16 @@ def run(cfg: SWConfig, engine: str = "cuda", state: Optional[SWState] = None,
     step's row is copied back to pinned host memory as soon as the step is
     done (stream-ordered, no host synchronisation until the end).
     A host ``state`` is uploaded first; ``to_host=True`` returns the final
-    state as host Fields (written into ``out``'s arrays when given).
+    state as host Fields (written into ``out``'s arrays when given).  With a
+    host state, host output and a fixed dt on a large grid the upload, the
+    steps and the download overlap (fkc_sw_run_host: bands of rows stepped
+    as a wavefront while later bands are still crossing PCIe).
     """
     if engine not in ENGINES:
         raise ValueError(f"engine {engine!r} is not provided by the B200 package "
                          f"(available: {ENGINES}); the CPU engines live in the reference")
+    if state is not None and (to_host or out is not None) and _streamable(cfg, state, out):
+        return _run_streamed(cfg, state, out)
     sim = Simulation(cfg, state=state, diagnostics=True, stream_rows=True)
     sim.advance(cfg.steps)
     res = sim.rows()
