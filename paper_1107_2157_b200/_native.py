@@ -30,7 +30,9 @@ EXPORTS = (
     "fkc_tma_plan", "fkc_test_div_f32", "fkc_test_div_f64", "fkc_test_sqrt2_f32", "fkc_last_error",
     "fkc_abi_version",
 )
-ABI_VERSION = 3
+ABI_VERSION = 4
+SYNC_PDL = 1
+MAX_RANKS = 8
 
 
 class NativeUnavailable(RuntimeError):
@@ -70,9 +72,11 @@ class PeerLine(ctypes.Structure):
 
 
 class Sync(ctypes.Structure):
-    """fkc_sync: per-side mailbox words, edge-writer counters, epoch."""
+    """fkc_sync: per-side mailbox words, edge-writer counters, epoch, PDL flag, CFL board."""
     _fields_ = [("wait", ctypes.c_void_p * 4), ("signal", ctypes.c_void_p * 4),
-                ("counter", ctypes.c_void_p), ("epoch", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+                ("counter", ctypes.c_void_p), ("epoch", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("cfl_board", ctypes.c_void_p), ("cfl_peers", ctypes.c_void_p * 8), ("cfl_counter", ctypes.c_void_p),
+                ("cfl_rank", ctypes.c_int32), ("cfl_nranks", ctypes.c_int32)]
 
 
 class Tune(ctypes.Structure):

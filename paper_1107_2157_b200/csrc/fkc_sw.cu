@@ -87,6 +87,11 @@ SyncArgs to_sync(const fkc_sw_step_args* a) {
     }
     S.counter = a->sync.counter;
     S.epoch = a->sync.epoch;
+    S.board = (unsigned long long*)a->sync.cfl_board;
+    for (int r = 0; r < FKC_MAX_RANKS; ++r) S.peers[r] = (unsigned long long*)a->sync.cfl_peers[r];
+    S.ccount = a->sync.cfl_counter;
+    S.rank = a->sync.cfl_rank;
+    S.nranks = a->sync.cfl_board ? a->sync.cfl_nranks : 0;
     return S;
 }
 
@@ -103,6 +108,14 @@ int valid_peers(const fkc_sw_step_args* a) {
         for (int s = 0; s < 4; ++s)
             if ((y.wait[s] != nullptr) != (y.signal[s] != nullptr))
                 return fail(FKC_EUSAGE, "sync side %d: wait and signal must be given together", s);
+    }
+    if (y.flags & ~FKC_SYNC_PDL) return fail(FKC_EUSAGE, "sync.flags: unknown bits");
+    if (y.cfl_board) {
+        if (y.cfl_nranks < 1 || y.cfl_nranks > FKC_MAX_RANKS || y.cfl_rank < 0 || y.cfl_rank >= y.cfl_nranks)
+            return fail(FKC_EUSAGE, "sync: cfl_nranks must be 1..%d and cfl_rank < cfl_nranks", FKC_MAX_RANKS);
+        if (!y.cfl_counter) return fail(FKC_EUSAGE, "sync: cfl_counter missing");
+        for (int r = 0; r < y.cfl_nranks; ++r)
+            if (!y.cfl_peers[r]) return fail(FKC_EUSAGE, "sync: cfl_peers[%d] missing", r);
     }
     return FKC_OK;
 }
@@ -210,8 +223,9 @@ bool tma_eligible(const fkc_sw_step_args* a) {
 // Launch with programmatic dependent launch (see pdl_wait in sw_kernels.cuh).
 // `pdl` false: plain launch -- for grids below ~512^2 (B200, CUDA graphs: the
 // programmatic edge costs more than it hides, 256^2 fast 26 -> 20 Gcell/s)
-// and with the fused exchange (CTAs parked in griddepcontrol.wait must not
-// hold SMs a neighbour tile's kernel on the same GPU needs).
+// and with the fused exchange unless every neighbour tile runs on another
+// GPU (sync.flags FKC_SYNC_PDL): CTAs parked in griddepcontrol.wait must not
+// hold SMs a neighbour tile's kernel on the same GPU needs.
 template <class... KArgs, class... Args>
 void launch_step(void (*kern)(KArgs...), dim3 grd, dim3 blk, size_t smem, cudaStream_t st, bool pdl, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -236,7 +250,8 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     dim3 grd((g.nx + 63) / 64, (g.ny + 3) / 4);
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(red);
-    const bool pdl = !a->tune.no_pdl && (int64_t)g.nx * g.ny >= (1 << 18) && a->sync.counter == nullptr;
+    const bool pdl = !a->tune.no_pdl && (int64_t)g.nx * g.ny >= (1 << 18) &&
+                     (a->sync.counter == nullptr || (a->sync.flags & FKC_SYNC_PDL));
 #define GEN_ARGS g.nx, g.ny, g.pitch, (const T*)a->H, (const T*)a->U, (const T*)a->V, (T*)a->oH, (T*)a->oU, \
                  (T*)a->oV, T(a->dx), T(a->dy), dts, T(a->g), to_bcs(a->bc), red, to_peers(a), to_sync(a)
     if (fast) {
@@ -350,7 +365,9 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
     dim3 grd(p.nbands, p.nseg);
     SegMap sm = p.sm;
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
-    const bool pdl = !a->tune.no_pdl && a->sync.counter == nullptr;
+    // with the fused exchange only when the caller vouches that no neighbour
+    // tile shares this GPU (FKC_SYNC_PDL)
+    const bool pdl = !a->tune.no_pdl && (a->sync.counter == nullptr || (a->sync.flags & FKC_SYNC_PDL));
     launch_step(kern, grd, dim3(B::THREADS), B::SMEM_BYTES, st, pdl, m[0], m[1], m[2], g.nx,
                 g.ny, g.pitch, sm, a->tune.no_alternate ? 0 : 1, (T*)a->oH, (T*)a->oU, (T*)a->oV, (T)a->dx, (T)a->dy, dts, (T)a->g,
                 to_bcs(a->bc), to_red(a->red), to_peers(a), to_sync(a));

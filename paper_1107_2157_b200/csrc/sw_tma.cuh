@@ -456,7 +456,11 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         }
     }
     __syncwarp();
-    const T dt = resolve_dt<T>(dts);
+    // the rank boards only serve steps that also reduce the next bound (the
+    // SPEC run's CFL steps): other instantiations keep the plain path
+    T dt;
+    if constexpr (RED >= 2) dt = resolve_dt_sync<T>(dts, sy, lane, red.err);
+    else dt = resolve_dt<T>(dts);
     const Coef<T> c = make_coef<T>(dx, dy, dt, g);
     const T dmin = dx < dy ? dx : dy;
     const int X = xs + CPL * lane;             // full column of cell 0 of this lane
@@ -670,7 +674,12 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         const int expected[4] = {(int)gridDim.y, (int)gridDim.y, nstrips, nstrips};
         if (lane == 0) peer_signal(sy, sides, expected);
     }
-    if constexpr (RED > 0) rr.commit(red, lane, dmin, fdep);
+    if constexpr (RED > 0) {
+        rr.commit(red, lane, dmin, fdep);
+        // decomposed SPEC run: the last committing warp publishes the tile's
+        // CFL bound to every rank's board
+        if (RED >= 2 && lane == 0) board_publish(sy, red.cfl_min, (uint32_t)(((nx - 1) / G::OWN + 1) * gridDim.y));
+    }
     return nstages;
 }
 
@@ -678,10 +687,11 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
 template <class T, bool FAST, int RED, int NW>
 __global__ void __launch_bounds__(NW * 32, tma::Blk<T, NW>::template ctas_per_sm<FAST, RED>())
 sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU,
-            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, SegMap sm, int alt,
+            const __grid_constant__ CUtensorMap tmV, int nx, int ny, int64_t pitch, const __grid_constant__ SegMap sm,
+            int alt,
             T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV,
             T dx, T dy, DtSrc dts, T g, const __grid_constant__ BCs bc, RedPtrs red,
-            const __grid_constant__ Peers P, SyncArgs sy) {
+            const __grid_constant__ Peers P, const __grid_constant__ SyncArgs sy) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
     const int warp = threadIdx.x >> 5;

@@ -303,8 +303,10 @@ class Mailbox:
         return self.ptr + 16
 
 
-def fill_sync(sync: "N.Sync", mail: Mailbox, signal: Dict[int, int], epoch: int):
-    """wait on our own mailbox words, signal the neighbours' words for us."""
+def fill_sync(sync: "N.Sync", mail: Mailbox, signal: Dict[int, int], epoch: int, pdl: bool = False):
+    """wait on our own mailbox words, signal the neighbours' words for us;
+    ``pdl``: every neighbour tile runs on another GPU (programmatic launch
+    stays on with the fused exchange)."""
     for s in (LEFT, RIGHT, DOWN, UP):
         if s in signal:
             sync.wait[s] = mail.word(s)
@@ -314,6 +316,7 @@ def fill_sync(sync: "N.Sync", mail: Mailbox, signal: Dict[int, int], epoch: int)
             sync.signal[s] = None
     sync.counter = mail.counters
     sync.epoch = epoch & 0xFFFFFFFF
+    sync.flags = N.SYNC_PDL if pdl else 0
 
 
 def initial_peer_exchange(grid: CartGrid, rank: int, st, lines: Dict[int, "N.PeerLine"], stream=None):
@@ -357,9 +360,20 @@ class PeerExchange:
         world = dist.get_world_size(group)
         # every failure is agreed on collectively, so all ranks raise together
         # (PeerSetupError) and a caller can fall back to another transport
+        # the CFL board of the decomposed SPEC run (include/fkc_sw.h fkc_sync):
+        # [2 parities][world] entries of {bound bits, tag}, written by every rank
+        import torch
+        self.world = world
+        self.board = torch.zeros(4 * world, dtype=torch.int64, device=dev)
+        self.board_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        try:
+            uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        except Exception:  # noqa: BLE001 - older torch: treat as shared (no PDL)
+            uuid = None
         try:
             mine, err = {"bufs": [[N.ipc_export(p) for p in _field_ptrs(b)] for b in bufs],
-                         "mail": N.ipc_export(self.mail.ptr),
+                         "mail": N.ipc_export(self.mail.ptr), "board": N.ipc_export(self.board.data_ptr()),
+                         "uuid": uuid,
                          "pitch": bufs[0].H.pitch, "itemsize": bufs[0].H.storage.element_size()}, None
         except Exception as e:  # noqa: BLE001 - reported collectively
             mine, err = None, f"rank {rank} export: {e}"
@@ -385,8 +399,21 @@ class PeerExchange:
                     self.lines[p][s] = line
                 h, off = info["mail"]
                 self.signal[s] = self._open(h) + off + 4 * OPPOSITE[s]
+            # every rank's board (own: local memory)
+            self.boards = []
+            for r in range(world):
+                if r == rank:
+                    self.boards.append(self.board.data_ptr())
+                else:
+                    h, off = everyone[r]["info"]["board"]
+                    self.boards.append(self._open(h) + off)
         except Exception as e:  # noqa: BLE001 - reported collectively
             err = f"rank {rank} open: {e}"
+        # programmatic launch with the fused exchange only if no neighbour
+        # tile shares this GPU
+        my_uuid = everyone[rank]["info"]["uuid"]
+        self.pdl = my_uuid is not None and all(everyone[n]["info"]["uuid"] not in (None, my_uuid)
+                                               for n in self.nbr.values())
         errs = [None] * world
         dist.all_gather_object(errs, err, group=group)
         errs = [e for e in errs if e]
@@ -398,6 +425,18 @@ class PeerExchange:
         if handle not in self._opened:
             self._opened[handle] = N.ipc_open(handle)
         return self._opened[handle]
+
+    def fill_board(self, sync: "N.Sync", rank: int):
+        """The CFL board fields of fkc_sync (global CFL minimum without a
+        collective)."""
+        if self.world > N.MAX_RANKS:
+            raise ValueError(f"the CFL board serves up to {N.MAX_RANKS} ranks")
+        sync.cfl_board = self.board.data_ptr()
+        for r, p in enumerate(self.boards):
+            sync.cfl_peers[r] = p
+        sync.cfl_counter = self.board_count.data_ptr()
+        sync.cfl_rank = rank
+        sync.cfl_nranks = self.world
 
     def close(self):
         for base in self._opened.values():
@@ -433,21 +472,26 @@ class DistributedSimulation:
 
     ``cfg.dt`` fixed: the weak-scaling benchmark.  ``cfg.dt is None``: the
     SPEC ``run`` across GPUs -- every step's fused
-    reduction writes this tile's CFL bound into a device slot, one 8-byte
-    all-reduce (MIN, stream-ordered: no host synchronisation) makes it the
-    global bound, and the next step reads its dt from that slot on the
-    device.  ``diagnostics=True`` (implied by CFL mode) also keeps the per-step
+    reduction produces this tile's CFL bound; with ``cfl_exchange="board"``
+    (default with the peer transport) the last warp of the step kernel
+    writes it into every rank's board (NVLink peer stores) and the next step
+    kernel takes the minimum of the board entries on the device -- no
+    collective, no extra launch; ``"allreduce"``: one 8-byte all-reduce (MIN,
+    stream-ordered) into a device slot per step.  ``diagnostics=True`` (implied by CFL mode) also keeps the per-step
     mass / maxima / error words; :meth:`rows` combines them over the ranks.
     """
 
     def __init__(self, cfg, grid: CartGrid, rank: int, device=None, group=None, stream=None,
-                 transport: str = "peer", state=None, diagnostics: bool = False, capacity=None):
+                 transport: str = "peer", state=None, diagnostics: bool = False, capacity=None,
+                 cfl_exchange: str = "auto"):
         import torch
         import torch.distributed as dist
         from . import swdemo
         from .field import Field
         if transport not in ("peer", "nccl", "auto"):
             raise ValueError(f"unknown transport {transport!r}")
+        if cfl_exchange not in ("auto", "board", "allreduce"):
+            raise ValueError(f"unknown cfl_exchange {cfl_exchange!r}")
         self.fallback_reason = None
         self.transport = transport
         self.cfg, self.grid, self.rank = cfg, grid, rank
@@ -494,6 +538,12 @@ class DistributedSimulation:
             dist.barrier(group)
         self._group = group
         self.cfl = cfg.dt is None
+        # per-step global CFL minimum: through the rank boards inside the step
+        # kernels (peer transport, <= 8 ranks), else a stream-ordered all-reduce
+        board_ok = self.peer is not None and dist.get_world_size(group) <= N.MAX_RANKS
+        if cfl_exchange == "board" and not board_ok:
+            raise ValueError("cfl_exchange='board' needs the peer transport and <= 8 ranks")
+        self.cfl_exchange = "board" if (cfl_exchange != "allreduce" and board_ok) else "allreduce"
         self.diag = diagnostics or self.cfl
         self.slots = None
         if self.diag:
@@ -543,7 +593,9 @@ class DistributedSimulation:
                     out_parity = (self.n + 1) % 2
                     for s, line in self.peer.lines[out_parity].items():
                         a.peer[s] = line
-                    fill_sync(a.sync, self.peer.mail, self.peer.signal, self.n)
+                    fill_sync(a.sync, self.peer.mail, self.peer.signal, self.n, pdl=self.peer.pdl)
+                    if self.cfl and self.cfl_exchange == "board":
+                        self.peer.fill_board(a.sync, self.rank)
                     N.check(L.fkc_sw_step(ctypes.byref(a), sp))
                 else:
                     N.check(L.fkc_sw_step(ctypes.byref(a), sp))
@@ -551,7 +603,7 @@ class DistributedSimulation:
                 if cfg.dt is not None:
                     dst.t = src.t + float(cfg.dt)
                 self.n += 1
-                if self.cfl:
+                if self.cfl and self.cfl_exchange == "allreduce":
                     self._allreduce_bound(self.n)
         return self
 
@@ -572,6 +624,11 @@ class DistributedSimulation:
         err = torch.tensor(np.stack([e & 1, (e >> 1) & 1, (e >> 2) & 1]))   # OR of bits = MAX per bit
         dev = self.slots.buf.device if dist.get_backend(self._group) == "nccl" else "cpu"
         mass, mx, err = mass.to(dev), mx.to(dev), err.to(dev)
+        # the tiles' CFL bounds (bits of positive doubles: integer MIN = value
+        # MIN); with the board exchange each slot holds only its tile's bound
+        cb = torch.tensor(self.slots.buf[: self.n + 1, 3].cpu().numpy()).to(dev)
+        dist.all_reduce(cb, op=dist.ReduceOp.MIN, group=self._group)
+        d["cfl_min"] = cb.cpu().numpy().view(np.float64)
         dist.all_reduce(mass, op=dist.ReduceOp.SUM, group=self._group)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self._group)
         dist.all_reduce(err, op=dist.ReduceOp.MAX, group=self._group)

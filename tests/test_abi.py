@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(N.EXPORTS), (names, N.EXPORTS)
     for name in names:
         assert hasattr(L, name), name
-    assert L.fkc_abi_version() == N.ABI_VERSION == 3
+    assert L.fkc_abi_version() == N.ABI_VERSION == 4
 
 
 def test_usage_errors_without_gpu():

@@ -379,7 +379,7 @@ def test_peer_setup_error_is_collective():
     assert got == {0: "PeerSetupError with rank 0 and 1", 1: "PeerSetupError with rank 0 and 1"}, got
 
 
-def _cfl_worker(rank, world, port, px, py, nx, ny, steps, bc, q):
+def _cfl_worker(rank, world, port, px, py, nx, ny, steps, bc, q, cfl_exchange="auto"):
     import torch
     import torch.distributed as dist
 
@@ -393,7 +393,10 @@ def _cfl_worker(rank, world, port, px, py, nx, ny, steps, bc, q):
         grid = CartGrid(px, py, nx, ny, bc)
         cfg = swdemo.SWConfig(nx=nx, ny=ny, steps=steps, cfl_factor=0.9, boundary=bc, mode="exact",
                               variant="tma")
-        sim = DistributedSimulation(cfg, grid, rank, torch.device("cuda", 0), transport="peer")
+        sim = DistributedSimulation(cfg, grid, rank, torch.device("cuda", 0), transport="peer",
+                                    cfl_exchange=cfl_exchange)
+        assert sim.cfl_exchange == ("allreduce" if cfl_exchange == "allreduce" else "board")
+        assert not sim.peer.pdl                       # all ranks share GPU 0
         sim.advance(steps)
         rows = sim.rows()
         st = sim.state()
@@ -404,11 +407,14 @@ def _cfl_worker(rank, world, port, px, py, nx, ny, steps, bc, q):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cfl_exchange", ["board", "allreduce"])
 @pytest.mark.parametrize("px,py,bc", [(1, 2, "reflective"), (2, 2, "periodic")])
-def test_distributed_cfl_run_matches_single_domain(px, py, bc):
+def test_distributed_cfl_run_matches_single_domain(px, py, bc, cfl_exchange):
     """The SPEC run across processes: CFL dt recomputed every step from the
-    tiles' fused bounds, all-reduced (MIN) per step -- same dt series, state
-    bit-identical and mass within 1e-12 of the single-domain swdemo.run."""
+    tiles' fused bounds -- combined on the device through the rank boards
+    (the step kernels publish and read them over peer memory) or all-reduced
+    (MIN) per step -- same dt series, state bit-identical and mass within
+    1e-12 of the single-domain swdemo.run."""
     import torch.multiprocessing as mp
 
     from paper_1107_2157_b200 import swdemo
@@ -417,7 +423,7 @@ def test_distributed_cfl_run_matches_single_domain(px, py, bc):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_cfl_worker, args=(r, world, port, px, py, nx, ny, steps, bc, q))
+    procs = [ctx.Process(target=_cfl_worker, args=(r, world, port, px, py, nx, ny, steps, bc, q, cfl_exchange))
              for r in range(world)]
     for p in procs:
         p.start()
