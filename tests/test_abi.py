@@ -248,3 +248,30 @@ def test_integration_c_example_on_device(nx, ny, K, tmp_path):
     want = c_oracle.run_fixed(H, U, V, K, 1.0, 1.0, 0.05)
     for g, w in zip(got[3:], want):
         assert np.array_equal(g, w)
+
+
+def test_integration_python_binding_matches_header():
+    """INTEGRATION.md section 2 (the ctypes binding a maintainer of fkc would
+    add) executes against the built library, and every structure it declares
+    has the size and field offsets of the repo's own mirrors (which
+    test_struct_layout_matches_c checks against the C header)."""
+    md = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = md[md.index("## 2. The binding"):md.index("## 3.")]
+    code = re.search(r"```python\n(.*?)```", sec, flags=re.S).group(1)
+    ns = {}
+    old = os.environ.get("FKC_LIB")
+    os.environ["FKC_LIB"] = N.LIB_PATH
+    try:
+        exec(compile(code, "INTEGRATION.md", "exec"), ns)   # noqa: S102 -- the documented binding itself
+    finally:
+        if old is None:
+            os.environ.pop("FKC_LIB", None)
+        else:
+            os.environ["FKC_LIB"] = old
+    for name in ("Grid", "Reduce", "PeerLine", "Sync", "Tune", "StepArgs", "LoopArgs"):
+        mine, doc = getattr(N, name), ns[name]
+        assert ctypes.sizeof(doc) == ctypes.sizeof(mine), name
+        assert [f[0] for f in doc._fields_] == [f[0] for f in mine._fields_], name
+        for f in mine._fields_:
+            assert getattr(doc, f[0]).offset == getattr(mine, f[0]).offset, (name, f[0])
+    assert callable(ns["advance"]) and callable(ns["run_host"])
