@@ -62,6 +62,29 @@ def main():
     for ex, conc in (("pack", False), ("fused", False), ("fused", True)):
         cfg = swdemo.SWConfig(nx=480, ny=256, dt=0.05, boundary="periodic", mode="fast")
         run_local_decomposed(cfg, 2, 2, 3, exchange=ex, concurrent=conc)
+    # round 2 kernels: the resident cluster loop (DSMEM pushes, both buffers,
+    # CFL slots), the persistent TMA loop (step counters, grid arrival), the
+    # streamed host run (wave launches, staging unpack / pack, side-stream
+    # reduction)
+    for prec in ("f32", "f64"):
+        H, U, V = so.random_state(96, 70, prec, seed=5)
+        for mode in ("exact", "fast"):
+            for bc in ("reflective", "periodic"):
+                for dt in (None, 0.05):
+                    cfg = swdemo.SWConfig(nx=96, ny=70, steps=4, dt=dt, cfl_factor=0.5, precision=prec, mode=mode,
+                                          boundary=bc, variant="resident")
+                    st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, prec)) for a in (H, U, V)))
+                    swdemo.run(cfg, state=st)
+                    cfg = swdemo.SWConfig(nx=96, ny=70, steps=4, dt=dt, cfl_factor=0.5, precision=prec, mode=mode,
+                                          boundary=bc, variant="loop")
+                    st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, prec)) for a in (H, U, V)))
+                    swdemo.run(cfg, state=st)
+    H, U, V = so.random_state(256, 300, "f32", seed=6)
+    for steps in (0, 3, 40):
+        hst = swdemo.SWState(*(Field.from_array(a, "f32") for a in (H, U, V)))
+        out = swdemo.SWState(*(Field.from_array(np.zeros_like(a), "f32") for a in (H, U, V)))
+        cfg = swdemo.SWConfig(nx=256, ny=300, steps=steps, dt=0.05)
+        swdemo._run_streamed(cfg, hst, out, band_rows=16)
     torch.cuda.synchronize()
     print("sanitize workload done")
 
