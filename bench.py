@@ -464,6 +464,12 @@ def extras_run(args, dev):
     return out
 
 
+def res_streamed(n, args) -> bool:
+    """Whether swdemo.run takes the streamed host path for the e2e call."""
+    from paper_1107_2157_b200 import swdemo
+    return n * n >= swdemo.STREAM_MIN_CELLS and args.variant in ("auto", "tma") and n % 4 == 0
+
+
 def e2e_run(n, dt, args, dev):
     """Same metric through the public API with HOST buffers, at the
     commanded --steps: the initial state is copied from pinned host memory,
@@ -508,6 +514,9 @@ def e2e_run(n, dt, args, dev):
             "h2d_bytes_per_step": round(state_bytes / args.steps, 1),
             "d2h_bytes_per_step": round((state_bytes + 40 * (args.steps + 1)) / args.steps, 1),
             "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
+            "path": "streamed host run (fkc_sw_run_host): 1-D staged band copies on two copy streams overlap the "
+                    "steps, which run band by band as a wavefront (one multi-band launch per band period) for the "
+                    "first / last up to 32 steps" if res_streamed(n, args) else "device loop (fkc_sw_advance_n)",
             "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel, each step's "
                            "40-byte row copied device->host after the step",
             "warm": "one untimed run() of the same call first (CUDA context, allocator, tensor maps)",

@@ -205,6 +205,22 @@ int main(int argc, char** argv) {
         cudaMemcpy2D(host, W * 4, ptr[(K % 2) ? 3 + i : i], pitch * 4, W * 4, Hh, cudaMemcpyDeviceToHost);
         fwrite(host, 4, n_host, o);
     }
+    /* the host-state run: pinned initial state in, K exact steps, pinned state out */
+    f = fopen(argv[1], "rb");
+    if (!f || fread(hdr, 4, 3, f) != 3) return 17;
+    float *hin[3], *hout[3];
+    for (int i = 0; i < 3; ++i) {
+        if (cudaMallocHost((void**)&hin[i], n_host * 4) != cudaSuccess) return 18;
+        if (cudaMallocHost((void**)&hout[i], n_host * 4) != cudaSuccess) return 18;
+        if (fread(hin[i], 4, n_host, f) != n_host) return 19;
+    }
+    fclose(f);
+    if (run_from_host(&t, K, (const float* const*)hin, hout, W * 4, 0) != FKC_OK) {
+        fprintf(stderr, "%s\n", fkc_last_error());
+        return 20;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return 21;
+    for (int i = 0; i < 3; ++i) fwrite(hout[i], 4, n_host, o);
     fclose(o);
     return 0;
 }
@@ -216,8 +232,9 @@ int main(int argc, char** argv) {
 def test_integration_c_example_on_device(nx, ny, K, tmp_path):
     """The INTEGRATION.md section 3 C example driven from a pure-C program
     on device memory it allocates itself (cudaMalloc, the padded layout):
-    one_step (fast mode) within the fast tolerance of the oracle, and the
-    native time loop many_steps (exact mode, K steps) bit-identical to it."""
+    one_step (fast mode) within the fast tolerance of the oracle, the native
+    time loop many_steps (exact mode, K steps) and the streamed host run
+    run_from_host (pinned host state in and out) bit-identical to it."""
     import numpy as np
     from oracle import c_oracle
     from oracle import sw_oracle as so
@@ -241,12 +258,14 @@ def test_integration_c_example_on_device(nx, ny, K, tmp_path):
     out = tmp_path / "out.bin"
     r = subprocess.run([str(exe), str(inp), str(out)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, (r.returncode, r.stderr)
-    got = np.fromfile(out, np.float32).reshape(6, ny + 2, nx + 2)
+    got = np.fromfile(out, np.float32).reshape(9, ny + 2, nx + 2)
     one = so.step(H, U, V, 1.0, 1.0, 0.05)
     for g, w in zip(got[:3], one):
         assert np.max(np.abs(g.astype(np.float64) - w)) <= 2e-5 * np.max(np.abs(w))
     want = c_oracle.run_fixed(H, U, V, K, 1.0, 1.0, 0.05)
-    for g, w in zip(got[3:], want):
+    for g, w in zip(got[3:6], want):
+        assert np.array_equal(g, w)
+    for g, w in zip(got[6:], want):          # run_from_host: the streamed host run, same bits
         assert np.array_equal(g, w)
 
 
