@@ -1135,9 +1135,15 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         cudaEventRecord(ev_done[i], st);
         cudaStreamWaitEvent(cs->down, ev_done[i], 0);
         for (int f = 0; f < 3; ++f) {
-            e = cudaMemcpyAsync((char*)host_out[f] + (int64_t)r_lo * host_pitch_bytes, slot + f * slot_field,
-                                (size_t)host_block(r_lo, r_hi), cudaMemcpyDeviceToHost, cs->down);
-            if (e != cudaSuccess) return fail(FKC_ECUDA, "cudaMemcpyAsync (download %d): %s", i, cudaGetErrorString(e));
+            char* dst = (char*)host_out[f] + (int64_t)r_lo * host_pitch_bytes;
+            // rows padded beyond the row length: a pitched copy, so the
+            // caller's padding is never written
+            e = host_pitch_bytes == row_b
+                    ? cudaMemcpyAsync(dst, slot + f * slot_field, (size_t)host_block(r_lo, r_hi),
+                                      cudaMemcpyDeviceToHost, cs->down)
+                    : cudaMemcpy2DAsync(dst, host_pitch_bytes, slot + f * slot_field, host_pitch_bytes, row_b,
+                                        r_hi - r_lo + 1, cudaMemcpyDeviceToHost, cs->down);
+            if (e != cudaSuccess) return fail(FKC_ECUDA, "device-to-host copy (band %d): %s", i, cudaGetErrorString(e));
         }
         cudaEventRecord(ev_dl[i], cs->down);
         return FKC_OK;

@@ -132,3 +132,38 @@ def test_streamed_errors():
     st = host_state(H, U, V)
     with pytest.raises(swdemo.LaunchError):
         swdemo._run_streamed(swdemo.SWConfig(nx=510, ny=64, steps=3, dt=0.04), st, empty_like_state(st))
+
+
+def test_run_host_c_abi_padded_host_pitch():
+    """fkc_sw_run_host through the C-ABI with host rows padded beyond the
+    row length (host pitch 37 elements past nx+2): same bits as the device
+    run; the padding is never written."""
+    import ctypes
+
+    import torch
+
+    from paper_1107_2157_b200 import _native as N
+    from paper_1107_2157_b200 import swdemo
+    nx, ny, pad = 384, 700, 37
+    H, U, V = so.random_state(nx, ny, "f32", seed=12)
+    hp = nx + 2 + pad
+    bufs_in = [torch.full((ny + 2, hp), -7.0, dtype=torch.float32, pin_memory=True) for _ in range(3)]
+    bufs_out = [torch.full((ny + 2, hp), -7.0, dtype=torch.float32, pin_memory=True) for _ in range(3)]
+    for b, a in zip(bufs_in, (H, U, V)):
+        b[:, :nx + 2] = torch.from_numpy(a)
+    st = host_state(H, U, V)
+    cfg = swdemo.SWConfig(nx=nx, ny=ny, steps=7, dt=0.04)
+    dev = swdemo.SWState(*(swdemo.DeviceField(st.full, "f32") for _ in range(3)), 9.8, 1.0, 0.8)
+    oth = swdemo.SWState(*(f.empty_like() for f in (dev.H, dev.U, dev.V)), 9.8, 1.0, 0.8)
+    L = N.LoopArgs()
+    L.step = swdemo._step_args(dev, oth, 0.04, "reflective", "exact", "auto")
+    L.steps = 7
+    src = (ctypes.c_void_p * 3)(*(b.data_ptr() for b in bufs_in))
+    dst = (ctypes.c_void_p * 3)(*(b.data_ptr() for b in bufs_out))
+    s = torch.cuda.current_stream()
+    N.check(N.lib().fkc_sw_run_host(ctypes.byref(L), src, dst, hp * 4, 48, s.cuda_stream))
+    s.synchronize()
+    _, want = device_run(cfg, st)
+    for b, w in zip(bufs_out, want):
+        assert np.array_equal(b[:, :nx + 2].numpy(), w)
+        assert bool((b[:, nx + 2:] == -7.0).all())
