@@ -167,3 +167,19 @@ def test_run_host_c_abi_padded_host_pitch():
     for b, w in zip(bufs_out, want):
         assert np.array_equal(b[:, :nx + 2].numpy(), w)
         assert bool((b[:, nx + 2:] == -7.0).all())
+
+
+@pytest.mark.parametrize("nx,ny,steps,band", [(128, 5, 3, 0), (4, 40, 6, 16), (8, 1, 2, 0), (256, 33, 40, 16)])
+def test_streamed_tiny_and_thin_grids(nx, ny, steps, band):
+    """Grids thinner than one band, one-row grids, a 4-column grid, and a run
+    longer than both wavefronts on a 3-band grid: same bits as the device run."""
+    from paper_1107_2157_b200 import swdemo
+    H, U, V = so.random_state(nx, ny, "f32", seed=nx + ny)
+    st = host_state(H, U, V)
+    cfg = swdemo.SWConfig(nx=nx, ny=ny, steps=steps, dt=0.04)
+    out = empty_like_state(st)
+    res = swdemo._run_streamed(cfg, st, out, band_rows=band)
+    want_res, want = device_run(cfg, st)
+    for x, w in zip((out.H.data, out.U.data, out.V.data), want):
+        assert np.array_equal(x, w)
+    assert np.array_equal(res.dts, want_res.dts)
