@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(res_warps<T, FAST>() * 32, 1) sw_resident(cons
     auto band_rows = [&](int bb) { return base + (bb < extra ? 1 : 0); };
     const ResGeo<T> L(nx, base + (extra ? 1 : 0));
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = tid & 31, warp = warp_index();   // provably warp-uniform (sw_tma.cuh)
     const T dx = T(a.dx), dy = T(a.dy), g = T(a.g), dmin = dx < dy ? dx : dy;
     const int below = b > 0 ? b - 1 : (a.bc.s[SIDE_D] == BC_PER ? nb - 1 : -1);
     const int above = b < nb - 1 ? b + 1 : (a.bc.s[SIDE_U] == BC_PER ? 0 : -1);

@@ -317,6 +317,16 @@ __device__ __noinline__ void edge_stores(T* oH, T* oU, T* oV, int64_t pitch, int
     }
 }
 
+// The warp's index in its CTA as a value the compiler can prove warp-uniform
+// (a lane-0 broadcast): with a plain threadIdx.x >> 5 it cannot for CTAs of
+// several warps, and every shuffle / vote after a branch on the strip (the
+// early exit of strips that own nothing) then compiles to a
+// WARPSYNC.COLLECTIVE fallback -- +20 % code in the sweep loop and 6-8 %
+// slower mid-size steps (measured).
+__device__ __forceinline__ int warp_index() {
+    return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+}
+
 // Persistent time loop (sw_loop_tma below): control block and the
 // neighbour ordering between its steps.
 // a loop has no peer tiles (zero-initialised constant bank: no local copy)
@@ -388,7 +398,7 @@ __device__ __forceinline__ void loop_nbr_wait(const LoopCtl& c, int strip, uint3
 // sw_loop_tma.  `kb` = ring stages the warp consumed before (mbarrier slot
 // and phase continue across the steps of a loop); returns the stages this
 // sweep consumed (0: the strip owns nothing).
-template <class T, bool FAST, int RED, int NW>
+template <class T, bool FAST, int RED, int NW, bool STEP = false>
 __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorMap* tmU, const CUtensorMap* tmV,
                                          int nx, int ny, int64_t pitch, const SegMap& sm, int alt,
                                          T* __restrict__ oH, T* __restrict__ oU, T* __restrict__ oV, T dx, T dy,
@@ -402,7 +412,7 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
     // OWN j, i.e. 480 j bytes) 16-byte aligned
     constexpr int DM = FAST ? DIV_FAST : DIV_GUARD;
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = warp_index();
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * NW + warp;
     const int xs = 1 + strip * G::OWN - CPL;             // full column of the first loaded column (ghost lane 0)
@@ -442,6 +452,17 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
 #ifndef FKC_LOOP_NOWAIT
 #define FKC_LOOP_NOWAIT 0     // timing experiments only (racy): skip the neighbour waits
 #endif
+    if constexpr (STEP) {
+        // the step kernel: programmatic launch and the ring's barriers here,
+        // after the geometry (the order the code generator handles best)
+        pdl_launch_dependents();
+        if (lane == 0) {
+            for (int s2 = 0; s2 < tma::S; ++s2) mbar_init(full + 8 * s2, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();                             // the barriers are initialised before any lane uses them
+        pdl_wait();                               // the previous step's output is complete
+    }
     if (lc && !FKC_LOOP_NOWAIT) loop_nbr_wait(*lc, strip, target, lane, red.err);
     if (lane == 0) {
         if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
@@ -451,7 +472,7 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         // ordered before the new TMA writes
         if (kb) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int k = 0; k < tma::S - 1 && k < nstages; ++k) {
-            const uint32_t sl = (kb + k) % tma::S;
+            const int sl = ((int)kb + k) % tma::S;
             issue_stage<T>(ring + sl * G::STAGE_BYTES, full + 8 * sl, tmH, tmU, tmV, tx, stage_y(k));
         }
     }
@@ -529,12 +550,12 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         return k < (nr + 2 + R - 1) / R;
     };
     for (int k = 0; stages_left(k); ++k) {
-        const uint32_t kg = kb + (uint32_t)k;          // ring stage index over the warp's lifetime
-        const int s = (int)(kg % tma::S);
+        const int kg = (int)kb + k;                    // ring stage index over the warp's lifetime
+        const int s = kg % tma::S;
         // refill the slot freed by stage k-1 (every lane finished reading it)
         if (lane == 0 && k + tma::S - 1 < nstages) {
             const int kn = k + tma::S - 1;
-            const uint32_t sl = (kb + (uint32_t)kn) % tma::S;
+            const int sl = ((int)kb + kn) % tma::S;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_stage<T>(ring + sl * G::STAGE_BYTES, full + 8 * sl, tmH, tmU, tmV, tx, stage_y(kn));
         }
@@ -694,17 +715,8 @@ sw_step_tma(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUt
             const __grid_constant__ Peers P, const __grid_constant__ SyncArgs sy) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
-    const int warp = threadIdx.x >> 5;
-    const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
-    pdl_launch_dependents();
-    if ((threadIdx.x & 31) == 0) {
-        for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();                                 // the barriers are initialised before any lane uses them
-    pdl_wait();                                   // the previous step's output is complete
-    tma_sweep<T, FAST, RED, NW>(&tmH, &tmU, &tmV, nx, ny, pitch, sm, alt, oH, oU, oV, dx, dy, dts, g, bc, red, P, sy,
-                                sbase, 0u);
+    tma_sweep<T, FAST, RED, NW, true>(&tmH, &tmU, &tmV, nx, ny, pitch, sm, alt, oH, oU, oV, dx, dy, dts, g, bc, red,
+                                      P, sy, sbase, 0u);
 }
 
 // ---------------------------------------------------------------------------
@@ -738,7 +750,7 @@ sw_wave_tma(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
     if ((int)blockIdx.y * w.seg >= tk.nyw) return;           // this task has fewer segments
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
-    const int warp = threadIdx.x >> 5;
+    const int warp = warp_index();
     const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
     if ((threadIdx.x & 31) == 0) {
         for (int s = 0; s < tma::S; ++s) mbar_init(full + 8 * s, 1);
@@ -794,7 +806,7 @@ sw_loop_tma(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
             const __grid_constant__ BCs bc, const __grid_constant__ LoopCtl ctl) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
-    const int warp = threadIdx.x >> 5;
+    const int warp = warp_index();
     const int lane = threadIdx.x & 31;
     const uint32_t full = sbase + NW * tma::Geo<T>::WARP_RING + warp * tma::S * 8;
     const int strip = blockIdx.x * NW + warp;
