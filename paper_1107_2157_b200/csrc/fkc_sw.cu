@@ -930,8 +930,17 @@ void wave_plan(const fkc_sw_step_args* a, int band_rows, int ntask, bool fast, i
                                    : (fast ? tma::Geo<T>::template warps_per_sm<true, 0>()
                                            : tma::Geo<T>::template warps_per_sm<false, 0>());
     const int nstrips = (a->grid.nx + tma::Geo<T>::OWN - 1) / tma::Geo<T>::OWN;
-    fkc_sw_tune t = a->tune;
-    seg = pick_seg((nstrips + nw - 1) / nw * ntask, band_rows, wps / nw, t);
+    (void)nstrips; (void)wps;
+    // a band splits into m = ceil(band / 30) segments of equal length, rounded
+    // up to 4k - 2 rows (no wasted row in a segment's last stage): 64-row
+    // bands take 22 + 22 + 20 instead of 30 + 30 + 4
+    if (a->tune.seg > 0) {
+        seg = a->tune.seg;
+        return;
+    }
+    const int m = (band_rows + 29) / 30;
+    const int even = (band_rows + m - 1) / m;
+    seg = ((even + 2 + 3) / 4) * 4 - 2;
 }
 
 template <class T>

@@ -43,7 +43,12 @@ namespace fkc {
 // per SM sub-partition); the fast pair engine and the f64 engines do not
 // without spills, so they run 8 warps (255 registers)
 constexpr int RES_MAX_WARPS = 12;
-template <class T, bool FAST> constexpr int res_warps() { return (FAST || sizeof(T) == 8) ? 8 : 12; }
+#ifndef FKC_RES_FAST_WARPS
+#define FKC_RES_FAST_WARPS 8
+#endif
+template <class T, bool FAST> constexpr int res_warps() {
+    return sizeof(T) == 8 ? 8 : (FAST ? FKC_RES_FAST_WARPS : 12);
+}
 constexpr int RES_MAX_CLUSTER = 16;
 #ifndef FKC_RES_FAST_UNROLL
 #define FKC_RES_FAST_UNROLL 2            // fast mode: rows of the sweep unrolled (register window renamed)
