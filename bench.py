@@ -238,7 +238,7 @@ def main():
     ap.add_argument("--no-other", action="store_true", help="skip the other-mode timing (profiling runs)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the BASELINE config 2 (4096^2 x 1000 steps) and grid-sweep (config 5b) lines")
-    ap.add_argument("--sweep", default="128,256,512,1024,2048,4096,8192,16384",
+    ap.add_argument("--sweep", default="16,32,64,128,256,512,1024,2048,4096,8192,16384",
                     help="grid sizes of the config-5b sweep reported under extras")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -406,9 +406,11 @@ def time_steps(st, n, dt, mode, variant, steps, warmup, sample_clocks=False, pre
 
 def extras_run(args, dev):
     """BASELINE config 2 (4096^2, 1000 steps, one native call per mode, after
-    10 warm-up steps) and the config-5b grid sweep 128^2 .. 16384^2 (fast
-    mode; each size's steps replayed from one CUDA graph), device-timed with
-    CUDA events.  Reported beside the headline, not as it."""
+    10 warm-up steps) and the config-5b grid sweep 16^2 .. 16384^2 -- the
+    paper's Table 1 widths 16 .. 4096 and beyond -- (fast
+    mode; each size's steps replayed from one CUDA graph: the small end runs
+    the resident cluster loop inside it), device-timed with CUDA events.
+    Reported beside the headline, not as it."""
     import torch
     from paper_1107_2157_b200 import swdemo
     out = {}
@@ -456,7 +458,8 @@ def extras_run(args, dev):
         ms = e0.elapsed_time(e1) / (reps * k)
         sweep.append({"n": n, "us_per_step": round(ms * 1e3, 3), "value": round(n * n / (ms / 1e3) / 1e9, 2),
                       "hbm_equiv_gbs": round(24 * n * n / (ms / 1e3) / 1e9, 1),
-                      "regime": "launch-bound" if n <= 512 else ("L2-resident" if n <= 2048 else "HBM")})
+                      "regime": ("resident (whole loop on chip)" if n <= 224 else "launch-bound") if n <= 512
+                      else ("L2-resident" if n <= 2048 else "HBM")})
         del sim, st
         torch.cuda.empty_cache()
     out["sweep_fast"] = {"unit": "Gcell-updates/s", "rows": sweep,
