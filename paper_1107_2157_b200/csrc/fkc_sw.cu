@@ -961,6 +961,9 @@ int launch_wave(const fkc_sw_step_args* a, const WaveArgs& w0, int band_rows, cu
 
 }  // extern "C++"
 
+#ifndef FKC_STREAM_COPY_ROWS
+#define FKC_STREAM_COPY_ROWS 256    // rows per host<->device copy of the streamed host run
+#endif
 // ---------------------------------------------------------------------------
 // streamed host run (fkc_sw_run_host): upload, steps and download overlapped
 // ---------------------------------------------------------------------------
@@ -1045,31 +1048,40 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     if (!tma_eligible(&s0)) return fail(FKC_EUSAGE, "fkc_sw_run_host: needs the TMA layout (nx, pitch, alignment)");
     cudaStream_t st = (cudaStream_t)stream;
     std::lock_guard<std::mutex> lk(g_cs_mu);     // the copy streams and events are per device, shared
-    // bands of ~band_rows interior rows (auto: 128 bands, >= 16 rows): the
-    // wavefront's lag is 2 bands per step, each launch carries a fixed cost
-    // (B200, 16384^2 x 20 steps, profiles/r02/stream_timing.txt: 64 rows
-    // 120 ms, 96 / 128 rows 98 / 99 ms, 256 rows 108 ms, 384 rows 121 ms)
-    int br = band_rows > 0 ? band_rows : (g.ny + 127) / 128;
+    // bands of ~band_rows interior rows (auto: 512 bands, >= 16 rows): the
+    // wavefront's lag is 2 bands per step, so thin bands shorten the head
+    // (upload only) and the tail (download only); the copies move several
+    // bands at once (B200, 16384^2 x 20 steps, profiles/r02/stream_timing.txt:
+    // 32 / 64 / 128-row bands 88.6 / 89.8 / 95.7 ms, the copies alone 81 ms)
+    int br = band_rows > 0 ? band_rows : (g.ny + 511) / 512;
     if (br < 16) br = 16;
     if (br > g.ny) br = g.ny;
     const int nb = (g.ny + br - 1) / br;
+    // copies move chunks of cb bands (~FKC_STREAM_COPY_ROWS rows): the copy
+    // engines reach both directions' full rate only with large transfers
+    int cb = FKC_STREAM_COPY_ROWS / br;
+    if (cb < 1) cb = 1;
+    if (cb > nb) cb = nb;
+    const int nc = (nb + cb - 1) / cb;
+    auto chunk_of = [&](int i) { return i / cb; };
     CopyStreams* cs = nullptr;
-    if (int rc = copy_streams(&cs, (size_t)5 * nb + 2)) return rc;
-    cudaEvent_t* ev_up = cs->ev.data();            // [nb]   chunk i in its upload staging slot
-    cudaEvent_t* ev_rep = cs->ev.data() + nb;      // [nb]   chunk i unpacked into the field (slot free)
-    cudaEvent_t* ev_done = cs->ev.data() + 2 * nb; // [nb]   band i final, packed into its download slot
-    cudaEvent_t* ev_dl = cs->ev.data() + 3 * nb;   // [nb]   band i downloaded (slot free)
-    cudaEvent_t* ev_red = cs->ev.data() + 4 * nb;  // [nb]   band i of the uploaded state reduced
-    cudaEvent_t ev_start = cs->ev[5 * nb], ev_end = cs->ev[5 * nb + 1];
+    if (int rc = copy_streams(&cs, (size_t)5 * nc + 2)) return rc;
+    cudaEvent_t* ev_up = cs->ev.data();            // [nc]   chunk c in its upload staging slot
+    cudaEvent_t* ev_rep = cs->ev.data() + nc;      // [nc]   chunk c unpacked into the field (slot free)
+    cudaEvent_t* ev_done = cs->ev.data() + 2 * nc; // [nc]   chunk c final, packed into its download slot
+    cudaEvent_t* ev_dl = cs->ev.data() + 3 * nc;   // [nc]   chunk c downloaded (slot free)
+    cudaEvent_t* ev_red = cs->ev.data() + 4 * nc;  // [nc]   chunk c of the uploaded state reduced
+    cudaEvent_t ev_start = cs->ev[5 * nc], ev_end = cs->ev[5 * nc + 1];
     const int64_t S = L->steps, f0 = L->first_step;
     const int64_t dpitch = g.pitch * es, row_b = (int64_t)(g.nx + 2) * es;
     const bool in_a = (f0 & 1) == 0, out_a = ((f0 + S) & 1) == 0;
     const void* A[3] = {s0.H, s0.U, s0.V};
     const void* Bf[3] = {s0.oH, s0.oU, s0.oV};
-    // full rows of chunk i: [r_lo, r_hi] (the halo rows travel with the first / last band)
-    auto chunk = [&](int i, int& r_lo, int& r_hi) {
-        r_lo = i == 0 ? 0 : 1 + i * br;
-        r_hi = i == nb - 1 ? g.ny + 1 : (i + 1) * br;
+    // full rows of copy chunk c: [r_lo, r_hi] (the halo rows travel with the
+    // first / last chunk)
+    auto chunk = [&](int c, int& r_lo, int& r_hi) {
+        r_lo = c == 0 ? 0 : 1 + c * cb * br;
+        r_hi = c == nc - 1 ? g.ny + 1 : (c + 1) * cb * br;
     };
     auto band = [&](int i, int& lo, int& n) {
         lo = 1 + i * br;
@@ -1084,7 +1096,7 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     // round for downloads); NS slots per direction, reused behind events.
     constexpr int NS = 16;
     const int64_t hp_el = host_pitch_bytes / es;
-    const int64_t slot_field = (int64_t)(br + 2) * host_pitch_bytes;
+    const int64_t slot_field = (int64_t)(cb * br + 2) * host_pitch_bytes;
     const int64_t slot_bytes = 3 * slot_field;
     // the previous call may still use the staging slots
     cudaStreamWaitEvent(st, cs->last, 0);
@@ -1152,7 +1164,7 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                                       cudaMemcpyDeviceToHost, cs->down)
                     : cudaMemcpy2DAsync(dst, host_pitch_bytes, slot + f * slot_field, host_pitch_bytes, row_b,
                                         r_hi - r_lo + 1, cudaMemcpyDeviceToHost, cs->down);
-            if (e != cudaSuccess) return fail(FKC_ECUDA, "device-to-host copy (band %d): %s", i, cudaGetErrorString(e));
+            if (e != cudaSuccess) return fail(FKC_ECUDA, "device-to-host copy (chunk %d): %s", i, cudaGetErrorString(e));
         }
         cudaEventRecord(ev_dl[i], cs->down);
         return FKC_OK;
@@ -1166,13 +1178,12 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     // diagnostics row of the uploaded state (row first_step), band by band as
     // the bands arrive, on a side stream (the step that overwrites band i of
     // the input buffer -- the run's second -- waits for it)
-    auto reduce_initial = [&](int i) -> int {
+    auto reduce_initial = [&](int c) -> int {
         if (!L->slots) return FKC_OK;
-        cudaStreamWaitEvent(cs->red, ev_rep[i], 0);
-        int lo, n;
-        band(i, lo, n);
+        cudaStreamWaitEvent(cs->red, ev_rep[c], 0);
+        const int lo = 1 + c * cb * br, hi = c == nc - 1 ? g.ny : (c + 1) * cb * br;
         fkc_grid sub = g;
-        sub.ny = n;
+        sub.ny = hi - lo + 1;
         const int64_t off = (int64_t)(lo - 1) * dpitch;
         fkc_sw_reduce red{};
         uint64_t* row = L->slots + 5 * f0;
@@ -1186,7 +1197,7 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         if (int rc = fkc_sw_reduce_state(&sub, base[0] + off, base[1] + off, base[2] + off, s0.dx, s0.dy, s0.g, &red,
                                          cs->red))
             return rc;
-        cudaEventRecord(ev_red[i], cs->red);
+        cudaEventRecord(ev_red[c], cs->red);
         return FKC_OK;
     };
     // the copy streams start after the caller's prior work
@@ -1218,9 +1229,10 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         const int lag = upload ? 1 : 0;
         const int64_t tmax = (int64_t)nb + 2 * (sb - sa) + 2;
         for (int64_t t = 0; t < tmax; ++t) {
-            if (upload && t < nb) {
-                if (int rc = upload_((int)t)) return rc;
-                if (int rc = reduce_initial((int)t)) return rc;
+            // the first step of band t-1 needs band t: its chunk arrives now
+            if (upload && t < nb && t % cb == 0) {
+                if (int rc = upload_((int)(t / cb))) return rc;
+                if (int rc = reduce_initial((int)(t / cb))) return rc;
             }
             WaveArgs w{};
             int64_t last_of[WAVE_MAX_TASKS];
@@ -1237,7 +1249,7 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 tk.red_row = L->slots ? (unsigned long long*)(L->slots + 5 * (gi + 1)) : nullptr;
                 last_of[w.ntask] = (i == nb - 1) ? sidx : -1;
                 ++w.ntask;
-                if (sidx == 1 && L->slots) cudaStreamWaitEvent(st, ev_red[i], 0);   // overwrites band i of the input
+                if (sidx == 1 && L->slots) cudaStreamWaitEvent(st, ev_red[chunk_of((int)i)], 0);   // overwrites band i
             }
             if (w.ntask == 0) continue;
             if (trace) {
@@ -1258,19 +1270,20 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 if (last_of[k] >= 0)
                     if (int rc2 = row_back(last_of[k])) return rc2;
             if (download) {
-                // the band whose last step ran in this launch: i = t - 2(sb-1-sa) - lag
+                // the band whose last step ran in this launch: i = t - 2(sb-1-sa) - lag;
+                // its chunk leaves once its last band is final
                 const int64_t i = t - 2 * (sb - 1 - sa) - lag;
-                if (i >= 0 && i < nb)
-                    if (int rc2 = download_((int)i)) return rc2;
+                if (i >= 0 && i < nb && (i == nb - 1 || (i + 1) % cb == 0))
+                    if (int rc2 = download_(chunk_of((int)i))) return rc2;
             }
         }
         return FKC_OK;
     };
     if (S == 0) {
-        for (int i = 0; i < nb; ++i) {
-            if (int rc = upload_(i)) return rc;
-            if (int rc = reduce_initial(i)) return rc;
-            if (int rc = download_(i)) return rc;
+        for (int c = 0; c < nc; ++c) {
+            if (int rc = upload_(c)) return rc;
+            if (int rc = reduce_initial(c)) return rc;
+            if (int rc = download_(c)) return rc;
         }
     } else {
         if (int rc = wavefront(0, s1, true, s2 == 0 && s3 == 0)) return rc;
@@ -1294,12 +1307,13 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         cudaEventSynchronize(ev_end);
         float te = 0.f;
         cudaEventElapsedTime(&te, ev_start, ev_end);
-        fprintf(stderr, "fkc_sw_run_host trace: %d bands of %d rows, %lld steps, end %.3f ms\n", nb, br, (long long)S, te);
-        for (int i = 0; i < nb; i += (nb > 16 ? nb / 16 : 1)) {
+        fprintf(stderr, "fkc_sw_run_host trace: %d bands of %d rows, copies of %d bands, %lld steps, end %.3f ms\n", nb,
+                br, cb, (long long)S, te);
+        for (int c = 0; c < nc; c += (nc > 16 ? nc / 16 : 1)) {
             float tu = -1.f, td = -1.f;
-            if (S > 0 && cudaEventQuery(ev_up[i]) == cudaSuccess) cudaEventElapsedTime(&tu, ev_start, ev_up[i]);
-            if (S > 0 && cudaEventQuery(ev_done[i]) == cudaSuccess) cudaEventElapsedTime(&td, ev_start, ev_done[i]);
-            fprintf(stderr, "  band %4d: uploaded %8.3f ms, last step done %8.3f ms\n", i, tu, td);
+            if (S > 0 && cudaEventQuery(ev_up[c]) == cudaSuccess) cudaEventElapsedTime(&tu, ev_start, ev_up[c]);
+            if (S > 0 && cudaEventQuery(ev_done[c]) == cudaSuccess) cudaEventElapsedTime(&td, ev_start, ev_done[c]);
+            fprintf(stderr, "  chunk %4d: uploaded %8.3f ms, last step done %8.3f ms\n", c, tu, td);
         }
         cudaDeviceSynchronize();
         for (size_t k = 0; k + 1 < trace_ev.size(); k += 2) {
