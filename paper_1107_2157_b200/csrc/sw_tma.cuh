@@ -449,9 +449,6 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         if (strip == 0) sides |= 1u << SIDE_L;
         if (G::OWN * (strip + 1) >= nx) sides |= 1u << SIDE_R;
     }
-#ifndef FKC_LOOP_NOWAIT
-#define FKC_LOOP_NOWAIT 0     // timing experiments only (racy): skip the neighbour waits
-#endif
     if constexpr (STEP) {
         // the step kernel: programmatic launch and the ring's barriers here,
         // after the geometry (the order the code generator handles best)
@@ -463,7 +460,7 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         __syncwarp();                             // the barriers are initialised before any lane uses them
         pdl_wait();                               // the previous step's output is complete
     }
-    if (lc && !FKC_LOOP_NOWAIT) loop_nbr_wait(*lc, strip, target, lane, red.err);
+    if (lc) loop_nbr_wait(*lc, strip, target, lane, red.err);
     if (lane == 0) {
         if (sides) peer_wait(sy, sides, red.err);   // before the first halo load
         // the neighbours' generic-proxy stores are read by TMA (async proxy)
@@ -844,10 +841,7 @@ sw_loop_tma(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUt
         kb += (uint32_t)n;
         __syncwarp();                                // every lane's stores (and reduction atomics) issued
         if (lane == 0) {
-#ifndef FKC_LOOP_WRITER_PROXY
-#define FKC_LOOP_WRITER_PROXY 1
-#endif
-            if (FKC_LOOP_WRITER_PROXY) asm volatile("fence.proxy.async.global;" ::: "memory");   // our stores, read by TMA next
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // our stores, read by TMA next
             if (cfl_loop) {
                 __threadfence();
                 // grid-wide arrival: the last warp of a sub-counter bumps the top
