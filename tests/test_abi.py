@@ -294,3 +294,77 @@ def test_integration_python_binding_matches_header():
         for f in mine._fields_:
             assert getattr(doc, f[0]).offset == getattr(mine, f[0]).offset, (name, f[0])
     assert callable(ns["advance"]) and callable(ns["run_host"])
+
+
+def test_round2_usage_errors_without_gpu():
+    """ABI 4 additions reject bad arguments before any device work: the CFL
+    board fields of fkc_sync, the PDL flag, and fkc_sw_run_host's argument
+    checks (CFL dt, periodic rows, host pitch, null pointers)."""
+    L = N.lib()
+    a = N.StepArgs()
+    a.grid = N.Grid(8, 8, 12, 0, 0)
+    a.H, a.U, a.V, a.oH, a.oU, a.oV = 1024, 2048, 3072, 4096, 5120, 6144
+    a.dx = a.dy = 1.0
+    a.sync.flags = 2                                    # unknown flag bit
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    assert b"flags" in L.fkc_last_error()
+    a.sync.flags = 0
+    a.sync.cfl_board = 8192
+    a.sync.cfl_nranks, a.sync.cfl_rank = 9, 0            # more ranks than the board holds
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    a.sync.cfl_nranks, a.sync.cfl_rank = 2, 2            # rank out of range
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    a.sync.cfl_rank = 1                                  # counter / peer boards missing
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    a.sync.cfl_counter = 12288
+    assert L.fkc_sw_step(ctypes.byref(a), None) == N.FKC_EUSAGE
+    assert b"cfl_peers" in L.fkc_last_error()
+    # fkc_sw_run_host
+    lp = N.LoopArgs()
+    lp.step = N.StepArgs()
+    lp.step.grid = N.Grid(8, 8, 12, 0, 0)
+    lp.step.H, lp.step.U, lp.step.V, lp.step.oH, lp.step.oU, lp.step.oV = 1024, 2048, 3072, 4096, 5120, 6144
+    lp.step.dx = lp.step.dy = 1.0
+    lp.steps = 2
+    vp3 = ctypes.c_void_p * 3
+    src, dst = vp3(64, 128, 192), vp3(256, 320, 384)
+    assert L.fkc_sw_run_host(None, src, dst, 40, 0, None) == N.FKC_EUSAGE
+    assert L.fkc_sw_run_host(ctypes.byref(lp), src, vp3(256, 0, 384), 40, 0, None) == N.FKC_EUSAGE
+    assert L.fkc_sw_run_host(ctypes.byref(lp), src, dst, 8, 0, None) == N.FKC_EUSAGE        # pitch < row
+    assert b"pitch" in L.fkc_last_error()
+    lp.dt_from_slots = 1
+    lp.slots = 4096
+    assert L.fkc_sw_run_host(ctypes.byref(lp), src, dst, 40, 0, None) == N.FKC_EUSAGE
+    assert b"fixed dt" in L.fkc_last_error()
+    lp.dt_from_slots = 0
+    lp.step.bc = N.bc_array((N.BC_REFLECTIVE, N.BC_REFLECTIVE, N.BC_PERIODIC, N.BC_PERIODIC))
+    assert L.fkc_sw_run_host(ctypes.byref(lp), src, dst, 40, 0, None) == N.FKC_EUSAGE
+    assert b"periodic" in L.fkc_last_error()
+
+
+def test_streamable_rules():
+    """swdemo.run's choice of the streamed host path (host state + host
+    output + fixed dt + non-periodic rows + the TMA layout + >= 2^20 cells,
+    contiguous host arrays of one pitch) -- host logic, no device."""
+    import numpy as np
+
+    from paper_1107_2157_b200 import swdemo
+    from paper_1107_2157_b200.field import Field
+
+    def st(nx, ny, order="C"):
+        return swdemo.SWState(*(Field.from_array(np.ones((ny + 2, nx + 2), np.float32, order=order), "f32")
+                                for _ in range(3)))
+    big = st(1024, 1024)
+    cfg = swdemo.SWConfig(nx=1024, ny=1024, steps=3, dt=0.05)
+    assert swdemo._streamable(cfg, big, None)
+    assert swdemo._streamable(cfg, big, st(1024, 1024))
+    assert not swdemo._streamable(swdemo.SWConfig(nx=1024, ny=1024, steps=3), big, None)          # CFL dt
+    assert not swdemo._streamable(swdemo.SWConfig(nx=1024, ny=1024, steps=3, dt=0.05, boundary="periodic"),
+                                  big, None)
+    assert not swdemo._streamable(swdemo.SWConfig(nx=1024, ny=1024, steps=3, dt=0.05, variant="generic"),
+                                  big, None)
+    assert not swdemo._streamable(cfg, st(1024, 1024, order="F"), None)                           # layout
+    small = swdemo.SWConfig(nx=512, ny=512, steps=3, dt=0.05)
+    assert not swdemo._streamable(small, st(512, 512), None)                                       # < 2^20 cells
+    odd = swdemo.SWConfig(nx=1026, ny=1024, steps=3, dt=0.05)
+    assert not swdemo._streamable(odd, st(1026, 1024), None)                                       # nx % 4
