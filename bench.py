@@ -436,6 +436,31 @@ def extras_run(args, dev):
         del sim, st
     out["config2_4096sq_1000_steps"] = {"unit": "Gcell-updates/s", **c2,
                                         "how": "one fkc_sw_advance_n call of 1000 steps, CUDA events"}
+    # BASELINE config 4's one-GPU base: 32768^2 (25.8 GB of state), fast mode
+    try:
+        n4 = 32768
+        st = device_gaussian_state(n4, n4, dev)
+        dt = 0.3 * swdemo.stable_dt(st, 1.0)
+        cfg = swdemo.SWConfig(nx=n4, ny=n4, steps=25, dt=dt, mode="fast")
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream)
+            sim.advance(5)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sim.advance(20)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out["config4_32768sq_1gpu"] = {"unit": "Gcell-updates/s", "value": round(n4 * n4 * 20 / (ms / 1e3) / 1e9, 2),
+                                       "us_per_step": round(ms / 20 * 1e3, 1),
+                                       "how": "20 steps after 5 warm-up, one fkc_sw_advance_n call, CUDA events; "
+                                              "the strong-scaling base of BASELINE config 4"}
+        del sim, st
+        torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001 - an extra, reported not fatal
+        out["config4_32768sq_1gpu"] = {"unavailable": str(e)[:120]}
     sweep = []
     for n in (int(x) for x in args.sweep.split(",") if x):
         st = device_gaussian_state(n, n, dev)
