@@ -840,13 +840,14 @@ struct GraphEntry {
 std::mutex g_graph_mu;
 std::vector<GraphEntry> g_graphs;
 
-// Chunked replay of the SPEC time loop (per-step reductions, CFL dt from the
-// device slots): the loop's launch-per-step host cost (~3-6 us on mid-size
-// grids, more than the step) goes away by replaying ONE captured graph of
-// FKC_CHUNK_STEPS steps.  The graph is position independent: its steps
-// reduce into a private ring of rows that a small kernel appends to the
-// caller's slots at a device step counter, so every chunk of the run (and
-// later runs on the same buffers) replays the same graph.
+// Chunked replay of an eager time loop (the SPEC run: per-step reductions,
+// CFL dt from the device slots; or plain fixed-dt steps): the loop's
+// launch-per-step host cost (~3-6 us, more than a small grid's step) goes
+// away by replaying ONE captured graph of FKC_CHUNK_STEPS steps.  The graph
+// is position independent: its steps reduce into a private ring of rows
+// that a small kernel appends to the caller's slots at a device step
+// counter, so every chunk of the run (and later runs on the same buffers)
+// replays the same graph.
 #ifndef FKC_CHUNK_STEPS
 #define FKC_CHUNK_STEPS 32
 #endif
@@ -871,10 +872,6 @@ static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
         fkc_sw_loop_args one = L;
         one.steps = 1;
         if (int rc = enqueue_loop(&one, st)) return rc;
-        if (L.host_slots) {
-            cudaMemcpyAsync(L.host_slots + 5 * (L.first_step + 1), L.slots + 5 * (L.first_step + 1),
-                            5 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
-        }
         L.first_step += 1;
         L.steps -= 1;
     }
@@ -891,11 +888,18 @@ static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
         for (auto& e : g_chunks)
             if (e.key == key) cg = &e;
         if (!cg) {
+            // with reduction slots: a ring of K+1 rows and the step counter
             ChunkGraph ng{key, nullptr, nullptr, nullptr};
-            if (cudaMalloc((void**)&ng.ring, 5 * sizeof(uint64_t) * (K + 1)) != cudaSuccess ||
-                cudaMalloc((void**)&ng.counter, sizeof(long long)) != cudaSuccess)
+            auto release = [&ng]() {
+                if (ng.ring) cudaFree(ng.ring);
+                if (ng.counter) cudaFree(ng.counter);
+            };
+            if (L.slots && (cudaMalloc((void**)&ng.ring, 5 * sizeof(uint64_t) * (K + 1)) != cudaSuccess ||
+                            cudaMalloc((void**)&ng.counter, sizeof(long long)) != cudaSuccess)) {
+                release();
                 return fail(FKC_ECUDA, "cudaMalloc (chunk ring)");
-            fkc_sw_loop_args lc = L;        // the chunk: K steps from an even step into the ring
+            }
+            fkc_sw_loop_args lc = L;        // the chunk: K steps from an even step (into the ring)
             lc.first_step = 0;
             lc.steps = K;
             lc.slots = (uint64_t*)ng.ring;
@@ -905,42 +909,57 @@ static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
             int dev = 0;
             cudaGetDevice(&dev);
             static cudaStream_t cap[64] = {};
-            if (dev < 0 || dev >= 64) return fail(FKC_EUSAGE, "device index %d", dev);
-            if (!cap[dev] && cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking) != cudaSuccess)
+            if (dev < 0 || dev >= 64) {
+                release();
+                return fail(FKC_EUSAGE, "device index %d", dev);
+            }
+            if (!cap[dev] && cudaStreamCreateWithFlags(&cap[dev], cudaStreamNonBlocking) != cudaSuccess) {
+                release();
                 return fail(FKC_ECUDA, "cudaStreamCreate (chunk capture)");
+            }
             cudaStream_t cs = cap[dev];
             cudaError_t err = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-            if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(err));
-            ring_reset_kernel<<<1, 64, 0, cs>>>(ng.ring, K);
+            if (err != cudaSuccess) {
+                release();
+                return fail(FKC_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(err));
+            }
+            if (L.slots) ring_reset_kernel<<<1, 64, 0, cs>>>(ng.ring, K);
             const int rc = enqueue_loop(&lc, cs);
-            ring_append_kernel<<<1, 256, 0, cs>>>(ng.ring, K, (unsigned long long*)L.slots, ng.counter);
+            if (L.slots) ring_append_kernel<<<1, 256, 0, cs>>>(ng.ring, K, (unsigned long long*)L.slots, ng.counter);
             cudaGraph_t graph = nullptr;
             err = cudaStreamEndCapture(cs, &graph);
-            if (rc) {
+            if (rc || err != cudaSuccess) {
                 if (graph) cudaGraphDestroy(graph);
-                return rc;
+                release();
+                return rc ? rc : fail(FKC_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(err));
             }
-            if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(err));
             err = cudaGraphInstantiate(&ng.exec, graph, 0);
             cudaGraphDestroy(graph);
-            if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(err));
+            if (err != cudaSuccess) {
+                release();
+                return fail(FKC_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(err));
+            }
             if (g_chunks.size() >= 8) {
-                cudaStreamSynchronize(st);
+                // the evicted graph may still run on another stream
+                cudaDeviceSynchronize();
                 cudaGraphExecDestroy(g_chunks.front().exec);
-                cudaFree(g_chunks.front().ring);
-                cudaFree(g_chunks.front().counter);
+                if (g_chunks.front().ring) cudaFree(g_chunks.front().ring);
+                if (g_chunks.front().counter) cudaFree(g_chunks.front().counter);
                 g_chunks.erase(g_chunks.begin());
             }
             g_chunks.push_back(ng);
             cg = &g_chunks.back();
         }
-        // the run's position: the input bound row and the step counter
-        cudaMemcpyAsync(cg->ring, L.slots + 5 * L.first_step, 5 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
-        set_counter_kernel<<<1, 1, 0, st>>>(cg->counter, (long long)L.first_step);
+        if (L.slots) {
+            // the run's position: the input bound row and the step counter
+            cudaMemcpyAsync(cg->ring, L.slots + 5 * L.first_step, 5 * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                            st);
+            set_counter_kernel<<<1, 1, 0, st>>>(cg->counter, (long long)L.first_step);
+        }
         for (int64_t c = 0; c < nchunks; ++c) {
             cudaError_t err = cudaGraphLaunch(cg->exec, st);
             if (err != cudaSuccess) return fail(FKC_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(err));
-            if (L.host_slots) {             // the host follows the run chunk by chunk
+            if (L.slots && L.host_slots) {  // the host follows the run chunk by chunk
                 const int64_t r = L.first_step + 1 + c * K;
                 cudaMemcpyAsync(L.host_slots + 5 * r, L.slots + 5 * r, 5 * sizeof(uint64_t) * K,
                                 cudaMemcpyDeviceToHost, st);
@@ -973,9 +992,10 @@ int fkc_sw_advance_n(const fkc_sw_loop_args* L, void* stream) {
         const int rc = try_loop(L, st);
         if (rc >= 0) return rc;
     }
-    // eager SPEC-style loops (per-step reductions) on grids where the launch
-    // per step costs about as much as the step: replay a chunk graph
-    if (!L->use_graph && L->slots && L->steps >= 4 * FKC_CHUNK_STEPS && !getenv("FKC_NO_CHUNK") &&
+    // eager loops (the SPEC run with per-step reductions, or plain fixed-dt
+    // steps) on grids where the launch per step costs about as much as the
+    // step: replay a chunk graph
+    if (!L->use_graph && L->steps >= 4 * FKC_CHUNK_STEPS && !getenv("FKC_NO_CHUNK") &&
         (int64_t)L->step.grid.nx * L->step.grid.ny <= FKC_CHUNK_MAX_CELLS) {
         cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(st, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusNone)

@@ -3,7 +3,8 @@
 diagnostics, one eager Simulation.advance call) per grid size: per-step time
 with the chunked graph replay (fkc_sw_advance_n run_chunked) against the
 launch-per-step loop (FKC_NO_CHUNK=1) and against a graph of fixed-dt steps without reductions
-(Simulation.capture, the floor).  Device-timed with CUDA events around the call.
+(Simulation.capture, the floor); and that fixed-dt loop through eager
+advance calls, chunked and per step.  Device-timed with CUDA events around the call.
 
     python scripts/chunk_timing.py [--sizes ..] [--modes exact,fast] [--prec f32] [--out FILE]
 """
@@ -63,12 +64,24 @@ def main():
                             os.environ.pop("FKC_NO_CHUNK", None)
                     # floor: the same steps at a fixed dt, no reductions, replayed from a graph
                     st0 = swdemo.init_state(cfg).to_device()
-                    fcfg = swdemo.SWConfig(nx=n, ny=n, dt=0.9 * swdemo.stable_dt(st0, 1.0), mode=mode, precision=prec)
+                    fcfg = swdemo.SWConfig(nx=n, ny=n, dt=0.3 * swdemo.stable_dt(st0, 1.0), mode=mode, precision=prec)
                     sim = swdemo.Simulation(fcfg, state=st0, diagnostics=False, stream=stream)
                     rep = sim.capture(k // 2)
                     rep()
                     row["graph_us"] = round(timed(rep, stream) / (k // 2) * 1e3, 3)
-                for key in ("chunk", "per_step", "graph"):
+                    # the same fixed-dt steps through eager advance calls
+                    for label, env in (("fixed_chunk", None), ("fixed_per_step", "1")):
+                        if env:
+                            os.environ["FKC_NO_CHUNK"] = env
+                        try:
+                            sim = swdemo.Simulation(fcfg, state=swdemo.init_state(cfg).to_device(),
+                                                    diagnostics=False, stream=stream)
+                            sim.advance(k)
+                            best = min(timed(lambda: sim.advance(k // 2), stream) for _ in range(2))
+                            row[f"{label}_us"] = round(best / (k // 2) * 1e3, 3)
+                        finally:
+                            os.environ.pop("FKC_NO_CHUNK", None)
+                for key in ("chunk", "per_step", "graph", "fixed_chunk", "fixed_per_step"):
                     row[f"{key}_gcell_s"] = round(n * n / row[f"{key}_us"] / 1e3, 2)
                 rows.append(row)
                 print(json.dumps(row), flush=True)

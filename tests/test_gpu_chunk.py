@@ -116,3 +116,24 @@ def test_chunked_run_many_simulations():
     want = run(H, U, V, (130,), False, cfl_factor=0.9)
     for _ in range(10):
         same(run(H, U, V, (130,), True, cfl_factor=0.9), want)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_chunked_fixed_dt_without_reductions(mode):
+    """An eager fixed-dt loop without diagnostics (no slots): 1 step, then
+    300 from an odd step, then 130; chunked equals per-step bit for bit."""
+    from paper_1107_2157_b200 import swdemo
+    H, U, V = so.random_state(480, 300, "f32", seed=11)
+    outs = []
+    for chunk in (True, False):
+        if not chunk:
+            os.environ["FKC_NO_CHUNK"] = "1"
+        try:
+            cfg = swdemo.SWConfig(nx=480, ny=300, dt=0.02, mode=mode)
+            sim = swdemo.Simulation(cfg, state=dev_state(H, U, V), diagnostics=False)
+            for k in (1, 300, 130):
+                sim.advance(k)
+            outs.append(host(sim.state()))
+        finally:
+            os.environ.pop("FKC_NO_CHUNK", None)
+    assert all(np.array_equal(x, y) for x, y in zip(*outs))
