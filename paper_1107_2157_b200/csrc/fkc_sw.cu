@@ -803,7 +803,9 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
 // ---------------------------------------------------------------------------
 // native time loop (+ cached CUDA graphs)
 // ---------------------------------------------------------------------------
-static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
+// row_words: the slot row stride (5 = the caller's layout; the chunk ring
+// uses RING_ROW)
+static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st, int row_words = 5) {
     fkc_sw_step_args a = L->step;
     const void* A[3] = {L->step.H, L->step.U, L->step.V};
     void* B[3] = {L->step.oH, L->step.oU, L->step.oV};
@@ -813,8 +815,8 @@ static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st) {
         a.H = even ? A[0] : B[0]; a.U = even ? A[1] : B[1]; a.V = even ? A[2] : B[2];
         a.oH = even ? B[0] : (void*)A[0]; a.oU = even ? B[1] : (void*)A[1]; a.oV = even ? B[2] : (void*)A[2];
         if (L->slots) {
-            uint64_t* in = L->slots + 5 * i;
-            uint64_t* out = L->slots + 5 * (i + 1);
+            uint64_t* in = L->slots + row_words * i;
+            uint64_t* out = L->slots + row_words * (i + 1);
             a.red.mass = (double*)out;
             a.red.max_abs_u = out + 1;
             a.red.max_abs_v = out + 2;
@@ -852,7 +854,7 @@ std::vector<GraphEntry> g_graphs;
 #define FKC_CHUNK_STEPS 32
 #endif
 #ifndef FKC_CHUNK_MAX_CELLS
-#define FKC_CHUNK_MAX_CELLS (4096 * 4096)
+#define FKC_CHUNK_MAX_CELLS (int64_t(1) << 40)
 #endif
 struct ChunkGraph {
     std::vector<unsigned char> key;
@@ -863,7 +865,7 @@ struct ChunkGraph {
 std::mutex g_chunk_mu;
 std::vector<ChunkGraph> g_chunks;
 
-static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st);
+static int enqueue_loop(const fkc_sw_loop_args* L, cudaStream_t st, int row_words);
 
 static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
     fkc_sw_loop_args L = *L0;
@@ -894,7 +896,7 @@ static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
                 if (ng.ring) cudaFree(ng.ring);
                 if (ng.counter) cudaFree(ng.counter);
             };
-            if (L.slots && (cudaMalloc((void**)&ng.ring, 5 * sizeof(uint64_t) * (K + 1)) != cudaSuccess ||
+            if (L.slots && (cudaMalloc((void**)&ng.ring, RING_ROW * sizeof(uint64_t) * (K + 1)) != cudaSuccess ||
                             cudaMalloc((void**)&ng.counter, sizeof(long long)) != cudaSuccess)) {
                 release();
                 return fail(FKC_ECUDA, "cudaMalloc (chunk ring)");
@@ -924,7 +926,7 @@ static int run_chunked(const fkc_sw_loop_args* L0, cudaStream_t st) {
                 return fail(FKC_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(err));
             }
             if (L.slots) ring_reset_kernel<<<1, 64, 0, cs>>>(ng.ring, K);
-            const int rc = enqueue_loop(&lc, cs);
+            const int rc = enqueue_loop(&lc, cs, RING_ROW);
             if (L.slots) ring_append_kernel<<<1, 256, 0, cs>>>(ng.ring, K, (unsigned long long*)L.slots, ng.counter);
             cudaGraph_t graph = nullptr;
             err = cudaStreamEndCapture(cs, &graph);

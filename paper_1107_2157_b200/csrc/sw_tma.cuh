@@ -477,8 +477,8 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
     // the rank boards only serve steps that also reduce the next bound (the
     // SPEC run's CFL steps): other instantiations keep the plain path
     T dt;
-    if constexpr (RED >= 2) dt = resolve_dt_sync<T>(dts, sy, lane, red.err);
-    else dt = resolve_dt<T>(dts);
+    if constexpr (RED >= 2) dt = resolve_dt_sync<T>(dts, sy, lane, red.err, lc != nullptr);
+    else dt = resolve_dt<T>(dts, lc != nullptr);
     const Coef<T> c = make_coef<T>(dx, dy, dt, g);
     const T dmin = dx < dy ? dx : dy;
     const int X = xs + CPL * lane;             // full column of cell 0 of this lane
@@ -696,7 +696,8 @@ __device__ __forceinline__ int tma_sweep(const CUtensorMap* tmH, const CUtensorM
         rr.commit(red, lane, dmin, fdep);
         // decomposed SPEC run: the last committing warp publishes the tile's
         // CFL bound to every rank's board
-        if (RED >= 2 && lane == 0) board_publish(sy, red.cfl_min, (uint32_t)(((nx - 1) / G::OWN + 1) * gridDim.y));
+        if (RED >= 2 && lane == 0 && sy.nranks > 0)
+            board_publish(sy, red.cfl_min, (uint32_t)(((nx - 1) / G::OWN + 1) * gridDim.y));
     }
     return nstages;
 }
