@@ -542,11 +542,11 @@ def e2e_run(n, dt, args, dev):
             "h2d_bytes_per_step": round(state_bytes / args.steps, 1),
             "d2h_bytes_per_step": round((state_bytes + 40 * (args.steps + 1)) / args.steps, 1),
             "api": "paper_1107_2157_b200.swdemo.run(cfg, state=<host pinned Fields>, out=<host pinned Fields>)",
-            "path": "streamed host run (fkc_sw_run_host): 1-D staged band copies on two copy streams overlap the "
+            "path": "streamed host run (fkc_sw_run_host): 1-D staged band copies (upload, pack and download streams) overlap the "
                     "steps, which run band by band as a wavefront (one multi-band launch per band period) for the "
                     "first / last up to 32 steps" if res_streamed(n, args) else "device loop (fkc_sw_advance_n)",
-            "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel, each step's "
-                           "40-byte row copied device->host after the step",
+            "diagnostics": "per-step mass/max|hu|/max|hv|/error word fused in the step kernel; the 40-byte "
+                           "rows copied device->host with the run (streamed run: once per wavefront phase)",
             "warm": "one untimed run() of the same call first (CUDA context, allocator, tensor maps)",
             "final_mass": res.rows[-1][3],
             "long_run_200_steps": {"value": round(long_value, 3), "seconds": round(long_el, 4),

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 #include <vector>
 #include <string>
@@ -1142,7 +1143,7 @@ fkc_sw_step_args step_of(const fkc_sw_loop_args* L, int64_t i) {
 }
 
 struct CopyStreams {
-    cudaStream_t up = nullptr, down = nullptr, red = nullptr;
+    cudaStream_t up = nullptr, down = nullptr, red = nullptr, pack = nullptr;
     std::vector<cudaEvent_t> ev;
     cudaEvent_t last = nullptr;      // end of the previous call (calls share the streams and the staging)
     char* stage = nullptr;           // staging slots, grow-only
@@ -1158,7 +1159,8 @@ int copy_streams(CopyStreams** out, size_t nev) {
     if (!c.up) {
         if (cudaStreamCreateWithFlags(&c.up, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&c.down, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&c.red, cudaStreamNonBlocking) != cudaSuccess)
+            cudaStreamCreateWithFlags(&c.red, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&c.pack, cudaStreamNonBlocking) != cudaSuccess)
             return fail(FKC_ECUDA, "cudaStreamCreate (copy streams)");
     }
     if (!c.last && cudaEventCreateWithFlags(&c.last, cudaEventDisableTiming) != cudaSuccess)
@@ -1199,7 +1201,11 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     // (upload only) and the tail (download only); the copies move several
     // bands at once (B200, 16384^2 x 20 steps, profiles/r02/stream_timing.txt:
     // 32 / 64 / 128-row bands 88.6 / 89.8 / 95.7 ms, the copies alone 81 ms)
-    int br = band_rows > 0 ? band_rows : (g.ny + 511) / 512;
+    // A run of at most 32 steps is one wavefront (upload and download):
+    // 1024 bands halve its lag (16384^2 x 20 steps: 82.2 -> 81.2 ms); longer
+    // runs keep 512 (their wavefront phases run faster on 32-row bands)
+    const int nbands_auto = L->steps <= 32 ? 1024 : 512;
+    int br = band_rows > 0 ? band_rows : (g.ny + nbands_auto - 1) / nbands_auto;
     if (br < 16) br = 16;
     if (br > g.ny) br = g.ny;
     const int nb = (g.ny + br - 1) / br;
@@ -1211,13 +1217,14 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     const int nc = (nb + cb - 1) / cb;
     auto chunk_of = [&](int i) { return i / cb; };
     CopyStreams* cs = nullptr;
-    if (int rc = copy_streams(&cs, (size_t)5 * nc + 2)) return rc;
+    if (int rc = copy_streams(&cs, (size_t)6 * nc + 3)) return rc;
     cudaEvent_t* ev_up = cs->ev.data();            // [nc]   chunk c in its upload staging slot
     cudaEvent_t* ev_rep = cs->ev.data() + nc;      // [nc]   chunk c unpacked into the field (slot free)
-    cudaEvent_t* ev_done = cs->ev.data() + 2 * nc; // [nc]   chunk c final, packed into its download slot
+    cudaEvent_t* ev_done = cs->ev.data() + 2 * nc; // [nc]   chunk c final (its last step done)
     cudaEvent_t* ev_dl = cs->ev.data() + 3 * nc;   // [nc]   chunk c downloaded (slot free)
     cudaEvent_t* ev_red = cs->ev.data() + 4 * nc;  // [nc]   chunk c of the uploaded state reduced
-    cudaEvent_t ev_start = cs->ev[5 * nc], ev_end = cs->ev[5 * nc + 1];
+    cudaEvent_t* ev_pk = cs->ev.data() + 5 * nc;   // [nc]   chunk c packed into its download slot
+    cudaEvent_t ev_start = cs->ev[6 * nc], ev_end = cs->ev[6 * nc + 1], ev_rows = cs->ev[6 * nc + 2];
     const int64_t S = L->steps, f0 = L->first_step;
     const int64_t dpitch = g.pitch * es, row_b = (int64_t)(g.nx + 2) * es;
     const bool in_a = (f0 & 1) == 0, out_a = ((f0 + S) & 1) == 0;
@@ -1286,21 +1293,28 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         cudaEventRecord(ev_rep[i], st);
         return FKC_OK;
     };
-    // download band i (its final state, compute-stream order): pack into slot
-    // i % NS (after the slot's previous band left), then D2H
+    // download chunk i once its rows are final (compute-stream order): pack
+    // into slot i % NS on the pack stream (after the slot's previous chunk
+    // left), D2H on the download stream.  The compute stream never waits for
+    // the downloads (a backlog would stall the last wavefront steps), and the
+    // packs run ahead of the D2H copies (no bubble between them).  The rows
+    // of a final chunk are only read from then on (later tasks write their
+    // own bands).
     auto download_ = [&](int i) -> int {
         int r_lo, r_hi;
         chunk(i, r_lo, r_hi);
         char* slot = stage_dn + (int64_t)(i % NS) * slot_bytes;
-        if (i >= NS) cudaStreamWaitEvent(st, ev_dl[i - NS], 0);
+        cudaEventRecord(ev_done[i], st);
+        cudaStreamWaitEvent(cs->pack, ev_done[i], 0);
+        if (i >= NS) cudaStreamWaitEvent(cs->pack, ev_dl[i - NS], 0);
         for (int f = 0; f < 3; ++f) {
             const char* dev = (const char*)(out_a ? A[f] : Bf[f]) + (int64_t)r_lo * dpitch;
             if (int rc = fkc_region_cpy(g.dtype, dev, g.nx + 2, r_hi - r_lo + 1, g.pitch, no_halo, slot + f * slot_field,
-                                        hp_el, st))
+                                        hp_el, cs->pack))
                 return rc;
         }
-        cudaEventRecord(ev_done[i], st);
-        cudaStreamWaitEvent(cs->down, ev_done[i], 0);
+        cudaEventRecord(ev_pk[i], cs->pack);
+        cudaStreamWaitEvent(cs->down, ev_pk[i], 0);
         for (int f = 0; f < 3; ++f) {
             char* dst = (char*)host_out[f] + (int64_t)r_lo * host_pitch_bytes;
             // rows padded beyond the row length: a pitched copy, so the
@@ -1351,6 +1365,7 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     cudaStreamWaitEvent(cs->up, ev_start, 0);
     cudaStreamWaitEvent(cs->down, ev_start, 0);
     cudaStreamWaitEvent(cs->red, ev_start, 0);
+    cudaStreamWaitEvent(cs->pack, ev_start, 0);
     // Phases: (1) the first P steps band by band as a wavefront behind the
     // upload (step s of band i after step s-1 of bands i-1 .. i+1 -- which also
     // covers the double buffer's write-after-read -- and after the upload of
@@ -1368,6 +1383,8 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
     // one launch are two bands apart, so none reads rows another writes.
     const bool trace = getenv("FKC_STREAM_TRACE") != nullptr;
     std::vector<cudaEvent_t> trace_ev;               // [launch start, launch end] pairs (trace mode)
+    std::vector<double> trace_host;                  // host time of each traced launch's enqueue (ms)
+    const auto host_t0 = std::chrono::steady_clock::now();
     fkc_sw_step_args a0 = s0;                       // H,U,V = buffer A, oH,oU,oV = buffer B
     a0.red = fkc_sw_reduce{};                       // per task (WaveTask::red_row)
     a0.dt_bound = nullptr;
@@ -1381,7 +1398,6 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 if (int rc = reduce_initial((int)(t / cb))) return rc;
             }
             WaveArgs w{};
-            int64_t last_of[WAVE_MAX_TASKS];
             for (int64_t sidx = sa; sidx < sb && w.ntask < WAVE_MAX_TASKS; ++sidx) {
                 const int64_t i = t - 2 * (sidx - sa) - lag;
                 if (i < 0 || i >= nb) continue;
@@ -1393,7 +1409,6 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 tk.ybase = lo;
                 tk.nyw = n;
                 tk.red_row = L->slots ? (unsigned long long*)(L->slots + 5 * (gi + 1)) : nullptr;
-                last_of[w.ntask] = (i == nb - 1) ? sidx : -1;
                 ++w.ntask;
                 if (sidx == 1 && L->slots) cudaStreamWaitEvent(st, ev_red[chunk_of((int)i)], 0);   // overwrites band i
             }
@@ -1403,6 +1418,8 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 cudaEventCreate(&e0);
                 cudaEventRecord(e0, st);
                 trace_ev.push_back(e0);
+                trace_host.push_back(
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count());
             }
             const int rc = g.dtype == FKC_F32 ? launch_wave<float>(&a0, w, br, st) : launch_wave<double>(&a0, w, br, st);
             if (rc) return rc;
@@ -1412,9 +1429,10 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 cudaEventRecord(e1, st);
                 trace_ev.push_back(e1);
             }
-            for (int k = 0; k < w.ntask; ++k)
-                if (last_of[k] >= 0)
-                    if (int rc2 = row_back(last_of[k])) return rc2;
+            // (the wavefront's diagnostics rows go back in one copy at its
+            // end: a 40-byte D2H per step on the compute stream queued behind
+            // the chunk downloads on the copy engine and stalled the steps --
+            // 2 ms each in the last wavefront)
             if (download) {
                 // the band whose last step ran in this launch: i = t - 2(sb-1-sa) - lag;
                 // its chunk leaves once its last band is final
@@ -1422,6 +1440,16 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
                 if (i >= 0 && i < nb && (i == nb - 1 || (i + 1) % cb == 0))
                     if (int rc2 = download_(chunk_of((int)i))) return rc2;
             }
+        }
+        if (L->slots && L->host_slots && sb > sa) {
+            // rows of steps sa .. sb-1, on the download stream after the last task
+            cudaEventRecord(ev_rows, st);
+            cudaStreamWaitEvent(cs->down, ev_rows, 0);
+            const int64_t r = f0 + sa + 1;
+            e = cudaMemcpyAsync(L->host_slots + 5 * r, L->slots + 5 * r, (size_t)(5 * sizeof(uint64_t) * (sb - sa)),
+                                cudaMemcpyDeviceToHost, cs->down);
+            if (e != cudaSuccess)
+                return fail(FKC_ECUDA, "cudaMemcpyAsync (diagnostics rows): %s", cudaGetErrorString(e));
         }
         return FKC_OK;
     };
@@ -1456,18 +1484,21 @@ int fkc_sw_run_host(const fkc_sw_loop_args* L, const void* const host_in[3], voi
         fprintf(stderr, "fkc_sw_run_host trace: %d bands of %d rows, copies of %d bands, %lld steps, end %.3f ms\n", nb,
                 br, cb, (long long)S, te);
         for (int c = 0; c < nc; c += (nc > 16 ? nc / 16 : 1)) {
-            float tu = -1.f, td = -1.f;
-            if (S > 0 && cudaEventQuery(ev_up[c]) == cudaSuccess) cudaEventElapsedTime(&tu, ev_start, ev_up[c]);
+            float tu = -1.f, td = -1.f, tl = -1.f;
+            if (cudaEventQuery(ev_up[c]) == cudaSuccess) cudaEventElapsedTime(&tu, ev_start, ev_up[c]);
             if (S > 0 && cudaEventQuery(ev_done[c]) == cudaSuccess) cudaEventElapsedTime(&td, ev_start, ev_done[c]);
-            fprintf(stderr, "  chunk %4d: uploaded %8.3f ms, last step done %8.3f ms\n", c, tu, td);
+            if (cudaEventQuery(ev_dl[c]) == cudaSuccess) cudaEventElapsedTime(&tl, ev_start, ev_dl[c]);
+            fprintf(stderr, "  chunk %4d: uploaded %8.3f ms, last step done %8.3f ms, downloaded %8.3f ms\n", c, tu,
+                    td, tl);
         }
         cudaDeviceSynchronize();
         for (size_t k = 0; k + 1 < trace_ev.size(); k += 2) {
-            if (k / 2 % 16 != 0) continue;
+            if (k / 2 % 16 != 0 && k / 2 + 60 < trace_ev.size() / 2) continue;
             float a = 0.f, b = 0.f;
             cudaEventElapsedTime(&a, ev_start, trace_ev[k]);
             cudaEventElapsedTime(&b, trace_ev[k], trace_ev[k + 1]);
-            fprintf(stderr, "  wave launch %4zu: starts %8.3f ms, runs %7.3f ms\n", k / 2, a, b);
+            fprintf(stderr, "  wave launch %4zu: starts %8.3f ms, runs %7.3f ms, enqueued %8.3f ms (host)\n", k / 2, a,
+                    b, trace_host[k / 2]);
         }
         for (auto e : trace_ev) cudaEventDestroy(e);
     }
