@@ -64,8 +64,8 @@ def main():
         run_local_decomposed(cfg, 2, 2, 3, exchange=ex, concurrent=conc)
     # round 2 kernels: the resident cluster loop (DSMEM pushes, both buffers,
     # CFL slots), the persistent TMA loop (step counters, grid arrival), the
-    # streamed host run (wave launches, staging unpack / pack, side-stream
-    # reduction)
+    # streamed host run (wave launches, staging unpack / pack on their own
+    # streams, side-stream reduction)
     for prec in ("f32", "f64"):
         H, U, V = so.random_state(96, 70, prec, seed=5)
         for mode in ("exact", "fast"):
@@ -85,6 +85,16 @@ def main():
         out = swdemo.SWState(*(Field.from_array(np.zeros_like(a), "f32") for a in (H, U, V)))
         cfg = swdemo.SWConfig(nx=256, ny=300, steps=steps, dt=0.05)
         swdemo._run_streamed(cfg, hst, out, band_rows=16)
+    # chunked time loops (captured 32-step graphs, reduction ring, append
+    # kernel): a CFL run and a fixed-dt run without reductions from an odd step
+    H, U, V = so.random_state(488, 120, "f32", seed=7)
+    for mode in ("exact", "fast"):
+        st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, "f32")) for a in (H, U, V)))
+        swdemo.run(swdemo.SWConfig(nx=488, ny=120, steps=130, cfl_factor=0.5, mode=mode), state=st)
+        st = swdemo.SWState(*(DeviceField.from_field(Field.from_array(a, "f32")) for a in (H, U, V)))
+        sim = swdemo.Simulation(swdemo.SWConfig(nx=488, ny=120, dt=0.02, mode=mode), state=st, diagnostics=False)
+        sim.advance(1)
+        sim.advance(129)
     torch.cuda.synchronize()
     print("sanitize workload done")
 
