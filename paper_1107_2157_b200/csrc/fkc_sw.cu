@@ -279,7 +279,13 @@ int sm_count() {
     return cached[dev];
 }
 
-int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
+// lean: an f32 fast-mode step with fused reductions on a grid of <= 2^22 cells.
+// Every segment ends in its reduction atomics and starts with the dt bound
+// read, so there fewer, longer segments win: >= 1.5 waves instead of 3 and
+// no guided tail (scripts/red_cost.py --seg/--warps sweep, CFL step: 1024^2
+// 13.6 -> 12.3 us, 2048^2 35.4 -> 32.0; 4096^2 and exact mode keep the
+// default schedule, which is best there).
+int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
     if (t.seg > 0) return t.seg;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
     // pipeline prologue; short ones shrink the tail of the last wave.  A
@@ -291,7 +297,7 @@ int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
     const int cands[5] = {30, 22, 14, 10, 6};
     const int64_t slots = (int64_t)sm_count() * ctas_per_sm;
     for (int seg : cands)
-        if ((int64_t)nbands * ((ny + seg - 1) / seg) >= 3 * slots) return seg;
+        if ((lean ? 2 : 1) * (int64_t)nbands * ((ny + seg - 1) / seg) >= 3 * slots) return seg;
     int best = 6;
     double best_fill = -1.0;
     for (int seg : cands) {
@@ -314,8 +320,9 @@ int seg_rev(const fkc_sw_tune& t) {
 
 // Guided segmentation: the last ~tail_waves waves of CTAs get short
 // segments of `tail` rows.
-SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t) {
-    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t), 0, 0, 0, 1, ny};
+SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t, lean), 0, 0, 0, 1, ny};
+    if (lean && t.tail_rows == 0) return m;
     // auto: about half the segment, again 4k - 2 rows (30 -> 14, 22 -> 10, 14 -> 6, 10 / 6 -> 2)
     const int tail = t.tail_rows == 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : t.tail_rows;
     if (tail <= 0 || tail >= m.seg || t.seg > 0) return m;
@@ -335,11 +342,11 @@ struct TmaPlan {
     int nbands, nseg;
     SegMap sm;
 };
-TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t) {
+TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
     TmaPlan p;
     const int nstrips = (nx + own - 1) / own;
     p.nbands = (nstrips + nw - 1) / nw;
-    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm, t);
+    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm, t, lean);
     const SegMap& m = p.sm;
     p.nseg = m.tail == 0 ? (ny + m.seg - 1) / m.seg : m.jt + (ny - m.jt * m.seg + m.tail - 1) / m.tail;
     return p;
@@ -360,7 +367,8 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
     if (nyw <= 0) { ybase = 1; nyw = g.ny; }
-    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune);
+    const bool lean = FAST && RED > 0 && sizeof(T) == 4 && (int64_t)g.nx * nyw <= (int64_t(1) << 22);
+    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune, lean);
     p.sm.rev = seg_rev(a->tune);
     p.sm.ybase = ybase;
     dim3 grd(p.nbands, p.nseg);
@@ -742,7 +750,8 @@ int fkc_tma_plan(const fkc_grid* g, int mode, int red_level, const fkc_sw_tune* 
                         : tma::Geo<float>::warps_per_sm<false, 0>();
     else wps = tma::Geo<double>::warps_per_sm<true, 0>();
     const int own = f32 ? tma::Geo<float>::OWN : tma::Geo<double>::OWN;
-    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw, t);
+    const bool lean = f32 && fast && red_level > 0 && (int64_t)g->nx * g->ny <= (int64_t(1) << 22);
+    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw, t, lean);
     out[0] = nw; out[1] = p.nbands; out[2] = p.nseg; out[3] = p.sm.seg; out[4] = p.sm.tail; out[5] = p.sm.jt;
     out[6] = wps / nw;
     return FKC_OK;

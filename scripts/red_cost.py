@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--modes", default="fast,exact")
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--combos", default="", help="comma list of combos to run (default all)")
+    ap.add_argument("--seg", type=int, default=0, help="tune.seg (rows per segment, 0 = auto)")
+    ap.add_argument("--warps", type=int, default=0, help="tune.warps (0 = auto)")
     ap.add_argument("--eager", type=int, default=0, help="N eager steps per combo instead of graph timing (profiling)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -55,7 +57,7 @@ def main():
             combos = {"none": {}, "err": dict(mass=False, maxima=False, cfl=False),
                       "err_mass": dict(maxima=False, cfl=False), "err_max": dict(mass=False, cfl=False),
                       "all": dict(cfl=False), "all_cfl": {}, "all_cfl_bound": {}, "all_cfl_bound_far": {}}
-            row = {"n": n, "mode": mode}
+            row = {"n": n, "mode": mode, "seg": args.seg, "warps": args.warps}
             for name, kw in combos.items():
                 if args.combos and name not in args.combos.split(","):
                     continue
@@ -66,6 +68,8 @@ def main():
                       for x, y in ((a, b), (b, a))]
                 for i, s in enumerate(sa):
                     s.tune.parity = i
+                    s.tune.seg = args.seg
+                    s.tune.warps = args.warps
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(s):
