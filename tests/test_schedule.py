@@ -74,3 +74,24 @@ def test_plan_tune_is_per_call():
     assert plan(16384)["seg"] == 30 and plan(16384)["warps"] == 4
     tail = plan(16384, tune=N.Tune(tail_rows=-1))
     assert tail["tail"] == 0 and tail["seg"] == 30
+
+
+@pytest.mark.parametrize("n", [512, 1024, 1448, 2048])
+@pytest.mark.parametrize("red", [1, 2])
+def test_plan_lean_for_reducing_fast_steps(n, red):
+    """f32 fast steps with fused reductions on grids of <= 2^22 cells take
+    fewer, longer segments (the longest giving >= 1.5 waves instead of 3)
+    and no guided tail; without reductions, in exact mode, in f64 or above
+    2^22 cells the default schedule stays (DESIGN.md 5.6 item 4)."""
+    p = plan(n, "fast", red)
+    assert p["tail"] == 0, p
+    slots = SM * p["ctas_per_sm"]
+    if 2 * p["bands"] * p["nseg"] >= 3 * slots:
+        for s in (30, 22, 14, 10, 6):
+            if s > p["seg"]:
+                assert 2 * p["bands"] * -(-n // s) < 3 * slots, (p, s)
+    if n >= 1024:
+        assert plan(n, "fast", 0)["tail"] > 0            # no reductions: guided tail
+        assert plan(n, "exact", red)["tail"] > 0 or plan(n, "exact", red)["seg"] == 6
+    assert plan(2896, "fast", red)["tail"] > 0           # above 2^22 cells: default schedule
+    assert plan(2048, "fast", red, prec="f64")["tail"] > 0 or plan(2048, "fast", red, prec="f64")["seg"] == 6
