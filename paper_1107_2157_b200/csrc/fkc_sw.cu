@@ -279,14 +279,21 @@ int sm_count() {
     return cached[dev];
 }
 
-// lean: an f32 fast-mode step with fused reductions on a grid of <= 2^22 cells.
+// SEG_LEAN: an f32 fast-mode step with fused reductions on a grid of <= 2^22 cells.
 // Every segment ends in its reduction atomics and starts with the dt bound
 // read, so there fewer, longer segments win: >= 1.5 waves instead of 3 and
 // no guided tail (scripts/red_cost.py --seg/--warps sweep, CFL step: 1024^2
 // 13.6 -> 12.3 us, 2048^2 35.4 -> 32.0; 4096^2 and exact mode keep the
 // default schedule, which is best there).
-int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
+// long: an f32 fast CFL step (RED 2) on a grid of > 2^26 cells -- its
+// per-segment commit and bound read favour long segments even there:
+// uniform 46-row segments (16384^2 CFL, 2-warp CTAs: 257.1 -> 260.4 Gcell/s;
+// the diagnostics-only and plain steps are best with the default).
+enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2 };
+int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     if (t.seg > 0) return t.seg;
+    if (shape == SEG_LONG) return 46;
+    const bool lean = shape == SEG_LEAN;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
     // pipeline prologue; short ones shrink the tail of the last wave.  A
     // segment loads seg + 2 rows in stages of R = 4, so seg = 4k - 2 wastes
@@ -320,9 +327,9 @@ int seg_rev(const fkc_sw_tune& t) {
 
 // Guided segmentation: the last ~tail_waves waves of CTAs get short
 // segments of `tail` rows.
-SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
-    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t, lean), 0, 0, 0, 1, ny};
-    if (lean && t.tail_rows == 0) return m;
+SegMap pick_segmap(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
+    SegMap m{pick_seg(nbands, ny, ctas_per_sm, t, shape), 0, 0, 0, 1, ny};
+    if (shape != SEG_DEFAULT && t.tail_rows == 0) return m;
     // auto: about half the segment, again 4k - 2 rows (30 -> 14, 22 -> 10, 14 -> 6, 10 / 6 -> 2)
     const int tail = t.tail_rows == 0 ? ((m.seg / 2 + 2) / 4) * 4 - 2 : t.tail_rows;
     if (tail <= 0 || tail >= m.seg || t.seg > 0) return m;
@@ -342,11 +349,17 @@ struct TmaPlan {
     int nbands, nseg;
     SegMap sm;
 };
-TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t, bool lean = false) {
+// the segment shape of an instantiation on a grid (row window) of `cells`
+int seg_shape(bool f32, bool fast, int red, int64_t cells) {
+    if (!f32 || !fast || red == 0) return SEG_DEFAULT;
+    if (cells <= (int64_t(1) << 22)) return SEG_LEAN;
+    return (red == 2 && cells > (int64_t(1) << 26)) ? SEG_LONG : SEG_DEFAULT;
+}
+TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     TmaPlan p;
     const int nstrips = (nx + own - 1) / own;
     p.nbands = (nstrips + nw - 1) / nw;
-    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm, t, lean);
+    p.sm = pick_segmap(p.nbands, ny, ctas_per_sm, t, shape);
     const SegMap& m = p.sm;
     p.nseg = m.tail == 0 ? (ny + m.seg - 1) / m.seg : m.jt + (ny - m.jt * m.seg + m.tail - 1) / m.tail;
     return p;
@@ -367,8 +380,8 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
     if (nyw <= 0) { ybase = 1; nyw = g.ny; }
-    const bool lean = FAST && RED > 0 && sizeof(T) == 4 && (int64_t)g.nx * nyw <= (int64_t(1) << 22);
-    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune, lean);
+    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune,
+                         seg_shape(sizeof(T) == 4, FAST, RED, (int64_t)g.nx * nyw));
     p.sm.rev = seg_rev(a->tune);
     p.sm.ybase = ybase;
     dim3 grd(p.nbands, p.nseg);
@@ -393,7 +406,10 @@ int pick_warps(const fkc_grid& g, bool fast, int red, const fkc_sw_tune& t) {
     if (t.warps) return t.warps;
     if (sizeof(T) == 8) return 1;
     const int64_t cells = (int64_t)g.nx * g.ny;
-    if (fast) return (red > 0 || cells < (3LL << 23)) ? 1 : 4;
+    // fast with fused reductions: 1-warp CTAs, 2-warp ones above 2^26 cells
+    // (round 2, reduction atomics fire-and-forget: 16384^2 CFL 252.7 -> 257.1,
+    // diagnostics 266.9 -> 268.0 Gcell/s; 8192^2 equal)
+    if (fast) return red > 0 ? (cells > (1LL << 26) ? 2 : 1) : (cells < (3LL << 23) ? 1 : 4);
     return cells < (1LL << 26) ? 1 : 2;
 }
 
@@ -750,8 +766,8 @@ int fkc_tma_plan(const fkc_grid* g, int mode, int red_level, const fkc_sw_tune* 
                         : tma::Geo<float>::warps_per_sm<false, 0>();
     else wps = tma::Geo<double>::warps_per_sm<true, 0>();
     const int own = f32 ? tma::Geo<float>::OWN : tma::Geo<double>::OWN;
-    const bool lean = f32 && fast && red_level > 0 && (int64_t)g->nx * g->ny <= (int64_t(1) << 22);
-    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw, t, lean);
+    const TmaPlan p = plan_tma(g->nx, g->ny, own, nw, wps / nw, t,
+                               seg_shape(f32, fast, red_level, (int64_t)g->nx * g->ny));
     out[0] = nw; out[1] = p.nbands; out[2] = p.nseg; out[3] = p.sm.seg; out[4] = p.sm.tail; out[5] = p.sm.jt;
     out[6] = wps / nw;
     return FKC_OK;

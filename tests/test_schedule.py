@@ -46,7 +46,10 @@ def test_plan_rules(n, mode, red, prec):
 
 def test_plan_choices():
     assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 30           # headline: 4-warp CTAs, 30-row segments
-    assert plan(16384, red=1)["warps"] == 1 and plan(16384, red=2)["warps"] == 1
+    assert plan(16384, red=1)["warps"] == 2 and plan(16384, red=2)["warps"] == 2     # > 2^26 cells
+    assert plan(8192, red=1)["warps"] == 1 and plan(8192, red=2)["warps"] == 1
+    assert plan(16384, red=2)["seg"] == 46 and plan(16384, red=2)["tail"] == 0        # long CFL segments
+    assert plan(16384, red=1)["seg"] == 30
     assert plan(2048)["warps"] == 1 and plan(4096)["warps"] == 1
     assert plan(16384, "exact")["warps"] == 2 and plan(4096, "exact")["warps"] == 1
     assert plan(16384, prec="f64")["warps"] == 1
