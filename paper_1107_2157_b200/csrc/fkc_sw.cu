@@ -285,7 +285,7 @@ int sm_count() {
 // no guided tail (scripts/red_cost.py --seg/--warps sweep, CFL step: 1024^2
 // 13.6 -> 12.3 us, 2048^2 35.4 -> 32.0; 4096^2 and exact mode keep the
 // default schedule, which is best there).
-// long: an f32 fast CFL step (RED 2) on a grid of > 2^26 cells -- its
+// SEG_LONG: an f32 CFL step (RED 2) on a grid of > 2^26 cells -- its
 // per-segment commit and bound read favour long segments even there:
 // uniform 46-row segments (16384^2 CFL, 2-warp CTAs: 257.1 -> 260.4 Gcell/s;
 // the diagnostics-only and plain steps are best with the default).
@@ -351,9 +351,9 @@ struct TmaPlan {
 };
 // the segment shape of an instantiation on a grid (row window) of `cells`
 int seg_shape(bool f32, bool fast, int red, int64_t cells) {
-    if (!f32 || !fast || red == 0) return SEG_DEFAULT;
-    if (cells <= (int64_t(1) << 22)) return SEG_LEAN;
-    return (red == 2 && cells > (int64_t(1) << 26)) ? SEG_LONG : SEG_DEFAULT;
+    if (!f32 || red == 0) return SEG_DEFAULT;
+    if (red == 2 && cells > (int64_t(1) << 26)) return SEG_LONG;   // exact too: 125.9 -> 127.6
+    return (fast && cells <= (int64_t(1) << 22)) ? SEG_LEAN : SEG_DEFAULT;
 }
 TmaPlan plan_tma(int nx, int ny, int own, int nw, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     TmaPlan p;

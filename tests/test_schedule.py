@@ -50,6 +50,7 @@ def test_plan_choices():
     assert plan(8192, red=1)["warps"] == 1 and plan(8192, red=2)["warps"] == 1
     assert plan(16384, red=2)["seg"] == 46 and plan(16384, red=2)["tail"] == 0        # long CFL segments
     assert plan(16384, red=1)["seg"] == 30
+    assert plan(16384, "exact", red=2)["seg"] == 46 and plan(16384, "exact", red=1)["seg"] == 30
     assert plan(2048)["warps"] == 1 and plan(4096)["warps"] == 1
     assert plan(16384, "exact")["warps"] == 2 and plan(4096, "exact")["warps"] == 1
     assert plan(16384, prec="f64")["warps"] == 1
