@@ -289,10 +289,18 @@ int sm_count() {
 // per-segment commit and bound read favour long segments even there:
 // uniform 46-row segments (16384^2 CFL, 2-warp CTAs: 257.1 -> 260.4 Gcell/s;
 // the diagnostics-only and plain steps are best with the default).
-enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2 };
+// SEG_HBM: the plain f32 fast step (no reductions) on a grid of >= 3*2^25
+// cells, launched eagerly: uniform 14-row segments (16 loaded rows = 4 whole
+// TMA stages) and no guided tail -- 16384^2 268.5 -> 278.2 Gcell/s, 32768^2
+// 273.6 -> 281.8, 11584^2 265 -> 272 (bench.py --seg sweep, round 2; DRAM
+// traffic stays 0.995x the algorithmic bytes, ncu); smaller grids, exact
+// mode, the reducing steps and captured launches keep their own schedules
+// (14-row segments cost them 4-15 %).
+enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3 };
 int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     if (t.seg > 0) return t.seg;
     if (shape == SEG_LONG) return 46;
+    if (shape == SEG_HBM) return 14;
     const bool lean = shape == SEG_LEAN;
     // Rows per CTA segment.  Long segments amortise the 2 halo rows and the
     // pipeline prologue; short ones shrink the tail of the last wave.  A
@@ -351,6 +359,7 @@ struct TmaPlan {
 };
 // the segment shape of an instantiation on a grid (row window) of `cells`
 int seg_shape(bool f32, bool fast, int red, int64_t cells) {
+    if (f32 && fast && red == 0 && cells >= (int64_t(3) << 25)) return SEG_HBM;
     if (!f32 || red == 0) return SEG_DEFAULT;
     if (red == 2 && cells > (int64_t(1) << 26)) return SEG_LONG;   // exact too: 125.9 -> 127.6
     return (fast && cells <= (int64_t(1) << 22)) ? SEG_LEAN : SEG_DEFAULT;
@@ -380,8 +389,20 @@ int launch_tma_t(const fkc_sw_step_args* a, cudaStream_t st, const CUtensorMap* 
         return fail(FKC_ECUDA, "cudaFuncSetAttribute(max dynamic smem): %s", cudaGetErrorString(attr_err));
     const fkc_grid& g = a->grid;
     if (nyw <= 0) { ybase = 1; nyw = g.ny; }
-    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune,
-                         seg_shape(sizeof(T) == 4, FAST, RED, (int64_t)g.nx * nyw));
+    int shape = seg_shape(sizeof(T) == 4, FAST, RED, (int64_t)g.nx * nyw);
+    if (shape == SEG_HBM) {
+        // inside a CUDA graph the 14-row segments lose 5 % against the
+        // default (scripts/seg_probe.py: 16384^2 graph 250 vs 264, eager
+        // 276 vs 268 Gcell/s): a captured launch keeps the default schedule
+        cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cst) != cudaSuccess) {
+            cudaGetLastError();               // (non-sticky) -- not this launch's error
+            shape = SEG_DEFAULT;
+        } else if (cst != cudaStreamCaptureStatusNone) {
+            shape = SEG_DEFAULT;
+        }
+    }
+    TmaPlan p = plan_tma(g.nx, nyw, G::OWN, NW, B::template ctas_per_sm<FAST, RED>(), a->tune, shape);
     p.sm.rev = seg_rev(a->tune);
     p.sm.ybase = ybase;
     dim3 grd(p.nbands, p.nseg);
@@ -880,7 +901,7 @@ std::vector<GraphEntry> g_graphs;
 #define FKC_CHUNK_STEPS 32
 #endif
 #ifndef FKC_CHUNK_MAX_CELLS
-#define FKC_CHUNK_MAX_CELLS (int64_t(1) << 40)
+#define FKC_CHUNK_MAX_CELLS (int64_t(1) << 24)   // above: the launch is noise, and eager launches take SEG_HBM
 #endif
 struct ChunkGraph {
     std::vector<unsigned char> key;

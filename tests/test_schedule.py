@@ -45,7 +45,9 @@ def test_plan_rules(n, mode, red, prec):
 
 
 def test_plan_choices():
-    assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 30           # headline: 4-warp CTAs, 30-row segments
+    assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 14           # headline: 4-warp CTAs, 14-row segments
+    assert plan(16384)["tail"] == 0 and plan(32768)["seg"] == 14 and plan(8192)["seg"] == 30
+    assert plan(16384, "exact")["seg"] == 30 and plan(16384, prec="f64")["seg"] != 14
     assert plan(16384, red=1)["warps"] == 2 and plan(16384, red=2)["warps"] == 2     # > 2^26 cells
     assert plan(8192, red=1)["warps"] == 1 and plan(8192, red=2)["warps"] == 1
     assert plan(16384, red=2)["seg"] == 46 and plan(16384, red=2)["tail"] == 0        # long CFL segments
@@ -72,12 +74,13 @@ def test_plan_usage_errors():
 def test_plan_tune_is_per_call():
     """The schedule knobs travel in the argument block (fkc_sw_tune), so one
     caller's forced schedule never leaks into another's (ABI 3)."""
-    forced = plan(16384, tune=N.Tune(seg=14, warps=2))
-    assert forced["seg"] == 14 and forced["warps"] == 2 and forced["tail"] == 0
+    forced = plan(16384, tune=N.Tune(seg=22, warps=2))
+    assert forced["seg"] == 22 and forced["warps"] == 2 and forced["tail"] == 0
     assert plan(16384) == plan(16384, tune=N.Tune())
-    assert plan(16384)["seg"] == 30 and plan(16384)["warps"] == 4
-    tail = plan(16384, tune=N.Tune(tail_rows=-1))
-    assert tail["tail"] == 0 and tail["seg"] == 30
+    assert plan(16384)["seg"] == 14 and plan(16384)["warps"] == 4
+    assert plan(8192, tune=N.Tune(tail_rows=-1))["tail"] == 0 and plan(8192)["tail"] > 0
+    tail = plan(8192, tune=N.Tune(tail_rows=-1))
+    assert tail["seg"] == 30
 
 
 @pytest.mark.parametrize("n", [512, 1024, 1448, 2048])
