@@ -48,6 +48,7 @@ def test_plan_choices():
     assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 14           # headline: 4-warp CTAs, 14-row segments
     assert plan(16384)["tail"] == 0 and plan(32768)["seg"] == 14 and plan(8192)["seg"] == 30
     assert plan(16384, "exact")["seg"] == 30 and plan(16384, prec="f64")["seg"] != 14
+    assert plan(16384, prec="f64")["tail"] == 0 and plan(16384, "exact", prec="f64")["tail"] == 0
     assert plan(16384, red=1)["warps"] == 2 and plan(16384, red=2)["warps"] == 2     # > 2^26 cells
     assert plan(8192, red=1)["warps"] == 1 and plan(8192, red=2)["warps"] == 1
     assert plan(16384, red=2)["seg"] == 46 and plan(16384, red=2)["tail"] == 0        # long CFL segments
