@@ -49,6 +49,9 @@ def test_plan_choices():
     assert plan(16384)["tail"] == 0 and plan(32768)["seg"] == 14 and plan(8192)["seg"] == 30
     assert plan(16384, "exact")["seg"] == 30 and plan(16384, prec="f64")["seg"] != 14
     assert plan(16384, prec="f64")["tail"] == 0 and plan(16384, "exact", prec="f64")["tail"] == 0
+    # exact, 2^25 .. 2^27 cells (eager): uniform segments giving >= 18 waves
+    assert plan(6144, "exact")["seg"] == 10 and plan(8192, "exact")["seg"] == 14
+    assert plan(6144, "exact")["tail"] == 0 and plan(4096, "exact")["tail"] > 0
     assert plan(16384, red=1)["warps"] == 2 and plan(16384, red=2)["warps"] == 2     # > 2^26 cells
     assert plan(8192, red=1)["warps"] == 1 and plan(8192, red=2)["warps"] == 1
     assert plan(16384, red=2)["seg"] == 46 and plan(16384, red=2)["tail"] == 0        # long CFL segments
