@@ -304,11 +304,15 @@ int sm_count() {
 // (bench.py --seg sweep: 6144^2 116.6 -> 129.0 (10 rows), 8192^2 134.8 ->
 // 142.4 (14 rows), 8192^2 diagnostics 127.3 -> 132.2, CFL 110.1 -> 111.5;
 // 11584^2 and 16384^2 unchanged, 4096^2 best with the default).
-enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3, SEG_NOTAIL = 4, SEG_FINE = 5 };
+// SEG_18: the plain f32 fast step on 2^26 .. 3*2^25 cells (8192^2 class):
+// uniform 18-row segments, eager or captured (8192^2 eager 255.5 -> 259.5,
+// graph 261.8 -> 266.7 Gcell/s).
+enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3, SEG_NOTAIL = 4, SEG_FINE = 5, SEG_18 = 6 };
 int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     if (t.seg > 0) return t.seg;
     if (shape == SEG_LONG) return 46;
     if (shape == SEG_HBM) return 14;
+    if (shape == SEG_18) return 18;
     if (shape == SEG_FINE) {
         const int64_t want = 18 * (int64_t)sm_count() * ctas_per_sm;
         for (int seg : {30, 22, 18, 14})
@@ -374,6 +378,7 @@ struct TmaPlan {
 // the segment shape of an instantiation on a grid (row window) of `cells`
 int seg_shape(bool f32, bool fast, int red, int64_t cells) {
     if (f32 && fast && red == 0 && cells >= (int64_t(3) << 25)) return SEG_HBM;
+    if (f32 && fast && red == 0 && cells >= (int64_t(1) << 26)) return SEG_18;
     if (!f32 && cells > (int64_t(1) << 26)) return SEG_NOTAIL;
     if (f32 && !fast && cells > (int64_t(1) << 25) && cells < (int64_t(1) << 27)) return SEG_FINE;
     if (!f32 || red == 0) return SEG_DEFAULT;
