@@ -307,12 +307,17 @@ int sm_count() {
 // SEG_18: the plain f32 fast step on 2^26 .. 3*2^25 cells (8192^2 class):
 // uniform 18-row segments, eager or captured (8192^2 eager 255.5 -> 259.5,
 // graph 261.8 -> 266.7 Gcell/s).
-enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3, SEG_NOTAIL = 4, SEG_FINE = 5, SEG_18 = 6 };
+// SEG_TINY: the plain f32 exact step below 2^20 cells: uniform 2-row
+// segments (one 4-row TMA stage per warp; 512^2 19.6 -> 36.3 Gcell/s, the
+// default's 6-row segments leave too few warps for the FMA-bound engine).
+enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3, SEG_NOTAIL = 4, SEG_FINE = 5, SEG_18 = 6,
+                SEG_TINY = 7 };
 int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
     if (t.seg > 0) return t.seg;
     if (shape == SEG_LONG) return 46;
     if (shape == SEG_HBM) return 14;
     if (shape == SEG_18) return 18;
+    if (shape == SEG_TINY) return 2;
     if (shape == SEG_FINE) {
         const int64_t want = 18 * (int64_t)sm_count() * ctas_per_sm;
         for (int seg : {30, 22, 18, 14})
@@ -381,6 +386,7 @@ int seg_shape(bool f32, bool fast, int red, int64_t cells) {
     if (f32 && fast && red == 0 && cells >= (int64_t(1) << 26)) return SEG_18;
     if (!f32 && cells > (int64_t(1) << 26)) return SEG_NOTAIL;
     if (f32 && !fast && cells > (int64_t(1) << 25) && cells < (int64_t(1) << 27)) return SEG_FINE;
+    if (f32 && !fast && red == 0 && cells < (int64_t(1) << 20)) return SEG_TINY;
     if (!f32 || red == 0) return SEG_DEFAULT;
     if (red == 2 && cells > (int64_t(1) << 26)) return SEG_LONG;   // exact too: 125.9 -> 127.6
     return (fast && cells <= (int64_t(1) << 22)) ? SEG_LEAN : SEG_DEFAULT;
@@ -853,9 +859,18 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     // parallelism wins -- B200 sweep (profiles/r01/variant_crossover.json):
     // 768^2 generic 85 / 43 vs TMA 43 (exact), 896^2 generic 92 / 45 vs TMA
     // 96 / 60, 1024^2 generic 98 / 46 vs TMA 112 / 71 Gcell/s (fast / exact)
-    if (variant == FKC_VARIANT_AUTO)
-        variant = tma_eligible(a) && (int64_t)a->grid.nx * a->grid.ny >= (int64_t(5) << 17) ? FKC_VARIANT_TMA
-                                                                                              : FKC_VARIANT_GENERIC;
+    //
+    // Round 2: the plain f32 exact step takes the TMA kernel from 2^18 cells,
+    // with 2-row segments below 2^20 (SEG_TINY): 512^2 29.9 -> 36.3,
+    // 640^2 39.6 -> 45.6, 768^2 42.7 -> 53.5 Gcell/s (graph replays).
+    if (variant == FKC_VARIANT_AUTO) {
+        const int64_t cells = (int64_t)a->grid.nx * a->grid.ny;
+        const bool plain_exact_f32 = a->mode == FKC_MODE_EXACT && a->grid.dtype == FKC_F32 &&
+                                     !any_red(to_red(a->red)) && a->dt_bound == nullptr;
+        variant = tma_eligible(a) && (cells >= (int64_t(5) << 17) || (plain_exact_f32 && cells >= (int64_t(1) << 18)))
+                      ? FKC_VARIANT_TMA
+                      : FKC_VARIANT_GENERIC;
+    }
     if (variant == FKC_VARIANT_TMA) {
         if (!tma_eligible(a))
             return fail(FKC_EUSAGE, "TMA variant needs nx and pitch multiples of 16/elem_size and (ptr+1 elem) "
