@@ -860,14 +860,15 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     // 768^2 generic 85 / 43 vs TMA 43 (exact), 896^2 generic 92 / 45 vs TMA
     // 96 / 60, 1024^2 generic 98 / 46 vs TMA 112 / 71 Gcell/s (fast / exact)
     //
-    // Round 2: the plain f32 exact step takes the TMA kernel from 2^18 cells,
-    // with 2-row segments below 2^20 (SEG_TINY): 512^2 29.9 -> 36.3,
-    // 640^2 39.6 -> 45.6, 768^2 42.7 -> 53.5 Gcell/s (graph replays).
+    // Round 2: the plain exact step takes the TMA kernel from 2^18 cells
+    // (f32, with 2-row segments below 2^20, SEG_TINY: 512^2 29.9 -> 36.3,
+    // 640^2 39.6 -> 45.6, 768^2 42.7 -> 53.5 Gcell/s) / 3*2^17 cells (f64:
+    // 640^2 19.5 -> 33.7, 768^2 21.0 -> 35.8), graph replays.
     if (variant == FKC_VARIANT_AUTO) {
         const int64_t cells = (int64_t)a->grid.nx * a->grid.ny;
-        const bool plain_exact_f32 = a->mode == FKC_MODE_EXACT && a->grid.dtype == FKC_F32 &&
-                                     !any_red(to_red(a->red)) && a->dt_bound == nullptr;
-        variant = tma_eligible(a) && (cells >= (int64_t(5) << 17) || (plain_exact_f32 && cells >= (int64_t(1) << 18)))
+        const bool plain_exact = a->mode == FKC_MODE_EXACT && !any_red(to_red(a->red)) && a->dt_bound == nullptr;
+        const int64_t exact_min = a->grid.dtype == FKC_F32 ? (int64_t(1) << 18) : (int64_t(3) << 17);
+        variant = tma_eligible(a) && (cells >= (int64_t(5) << 17) || (plain_exact && cells >= exact_min))
                       ? FKC_VARIANT_TMA
                       : FKC_VARIANT_GENERIC;
     }

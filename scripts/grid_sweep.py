@@ -21,6 +21,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="fast")
+    ap.add_argument("--precision", default="f32")
     ap.add_argument("--out", default=None)
     ap.add_argument("--sizes", default="128,256,512,1024,2048,4096,8192,16384")
     ap.add_argument("--segs", default="0", help="comma list of TMA segment lengths to try (0 = auto)")
@@ -47,9 +48,9 @@ def main():
             continue
         tr, tw = (int(x) for x in tail.split(":"))
         tune = N.Tune(warps=int(warps), no_pdl=1 - pdl, order=order, seg=seg, tail_rows=tr, tail_waves=tw)
-        st = device_gaussian_state(n, n, dev)
+        st = device_gaussian_state(n, n, dev, precision=args.precision)
         dt = 0.3 * swdemo.stable_dt(st, 1.0)
-        cfg = swdemo.SWConfig(nx=n, ny=n, dt=dt, mode=args.mode, variant=variant)
+        cfg = swdemo.SWConfig(nx=n, ny=n, dt=dt, mode=args.mode, variant=variant, precision=args.precision)
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
             sim = swdemo.Simulation(cfg, state=st, diagnostics=False, stream=stream, tune=tune)
