@@ -308,8 +308,9 @@ int sm_count() {
 // uniform 18-row segments, eager or captured (8192^2 eager 255.5 -> 259.5,
 // graph 261.8 -> 266.7 Gcell/s).
 // SEG_TINY: the plain f32 exact step below 2^20 cells: uniform 2-row
-// segments (one 4-row TMA stage per warp; 512^2 19.6 -> 36.3 Gcell/s, the
-// default's 6-row segments leave too few warps for the FMA-bound engine).
+// segments (one 4-row TMA stage per warp; 512^2 19.6 -> 36.3 Gcell/s on
+// the TMA kernel, the default's 6-row segments leave too few warps for the
+// FMA-bound engine).
 enum SegShape { SEG_DEFAULT = 0, SEG_LEAN = 1, SEG_LONG = 2, SEG_HBM = 3, SEG_NOTAIL = 4, SEG_FINE = 5, SEG_18 = 6,
                 SEG_TINY = 7 };
 int pick_seg(int nbands, int ny, int ctas_per_sm, const fkc_sw_tune& t, int shape = SEG_DEFAULT) {
@@ -861,9 +862,9 @@ int fkc_sw_step(const fkc_sw_step_args* a, void* stream) {
     // 96 / 60, 1024^2 generic 98 / 46 vs TMA 112 / 71 Gcell/s (fast / exact)
     //
     // Round 2: the plain exact step takes the TMA kernel from 2^18 cells
-    // (f32, with 2-row segments below 2^20, SEG_TINY: 512^2 29.9 -> 36.3,
-    // 640^2 39.6 -> 45.6, 768^2 42.7 -> 53.5 Gcell/s) / 3*2^17 cells (f64:
-    // 640^2 19.5 -> 33.7, 768^2 21.0 -> 35.8), graph replays.
+    // (f32, with 2-row segments below 2^20, SEG_TINY: 512^2 34.9 -> 37.0,
+    // 640^2 39.3 -> 45.6, 768^2 42.2 -> 53.5 Gcell/s) / 3*2^17 cells (f64:
+    // 640^2 19.5 -> 33.7, 768^2 20.9 -> 35.8), graph replays.
     if (variant == FKC_VARIANT_AUTO) {
         const int64_t cells = (int64_t)a->grid.nx * a->grid.ny;
         const bool plain_exact = a->mode == FKC_MODE_EXACT && !any_red(to_red(a->red)) && a->dt_bound == nullptr;
