@@ -298,11 +298,12 @@ int sm_count() {
 // (14-row segments cost them 4-15 %).
 // SEG_NOTAIL: f64 on > 2^26 cells -- the default length without the guided
 // tail (16384^2 fast 131.6-132.4 -> 133.9, exact 84.6 -> 85.5 Gcell/s).
-// SEG_FINE: the f32 exact step on 2^25 .. 2^27 cells, launched eagerly:
+// SEG_FINE: the f32 exact step on 23*2^20 .. 2^27 cells, launched eagerly:
 // uniform segments, the longest of 30/22/18/14/10 rows that still gives
 // >= 18 waves of CTAs -- many small CTAs balance the FMA-bound sweeps
 // (bench.py --seg sweep: 6144^2 116.6 -> 129.0 (10 rows), 8192^2 134.8 ->
-// 142.4 (14 rows), 8192^2 diagnostics 127.3 -> 132.2, CFL 110.1 -> 111.5;
+// 142.4 (14 rows), 5000^2 110.7 -> 118.6 (10 rows), 8192^2 diagnostics
+// 127.3 -> 132.2, CFL 110.1 -> 111.5;
 // 11584^2 and 16384^2 unchanged, 4096^2 best with the default).
 // SEG_18: the plain f32 fast step on 2^26 .. 3*2^25 cells (8192^2 class):
 // uniform 18-row segments, eager or captured (8192^2 eager 255.5 -> 259.5,
@@ -385,8 +386,11 @@ struct TmaPlan {
 int seg_shape(bool f32, bool fast, int red, int64_t cells) {
     if (f32 && fast && red == 0 && cells >= (int64_t(3) << 25)) return SEG_HBM;
     if (f32 && fast && red == 0 && cells >= (int64_t(1) << 26)) return SEG_18;
+    // (5000^2: uniform 14-row segments 224.6 -> 231.8 Gcell/s; 3584^2 and
+    // below keep the default)
+    if (f32 && fast && red == 0 && cells >= (int64_t(23) << 20)) return SEG_HBM;
     if (!f32 && cells > (int64_t(1) << 26)) return SEG_NOTAIL;
-    if (f32 && !fast && cells > (int64_t(1) << 25) && cells < (int64_t(1) << 27)) return SEG_FINE;
+    if (f32 && !fast && cells >= (int64_t(23) << 20) && cells < (int64_t(1) << 27)) return SEG_FINE;
     if (f32 && !fast && red == 0 && cells < (int64_t(1) << 20)) return SEG_TINY;
     if (!f32 || red == 0) return SEG_DEFAULT;
     if (red == 2 && cells > (int64_t(1) << 26)) return SEG_LONG;   // exact too: 125.9 -> 127.6

@@ -47,7 +47,7 @@ def test_plan_rules(n, mode, red, prec):
 def test_plan_choices():
     assert plan(16384)["warps"] == 4 and plan(16384)["seg"] == 14           # headline: 4-warp CTAs, 14-row segments
     assert plan(16384)["tail"] == 0 and plan(32768)["seg"] == 14 and plan(8192)["seg"] == 18
-    assert plan(8192)["tail"] == 0 and plan(6144)["seg"] == 30
+    assert plan(8192)["tail"] == 0 and plan(6144)["seg"] == 14 and plan(4096)["tail"] > 0
     assert plan(16384, "exact")["seg"] == 30 and plan(16384, prec="f64")["seg"] != 14
     assert plan(16384, prec="f64")["tail"] == 0 and plan(16384, "exact", prec="f64")["tail"] == 0
     # exact, 2^25 .. 2^27 cells (eager): uniform segments giving >= 18 waves
@@ -83,9 +83,9 @@ def test_plan_tune_is_per_call():
     assert forced["seg"] == 22 and forced["warps"] == 2 and forced["tail"] == 0
     assert plan(16384) == plan(16384, tune=N.Tune())
     assert plan(16384)["seg"] == 14 and plan(16384)["warps"] == 4
-    assert plan(6144, tune=N.Tune(tail_rows=-1))["tail"] == 0 and plan(6144)["tail"] > 0
-    tail = plan(6144, tune=N.Tune(tail_rows=-1))
-    assert tail["seg"] == 30
+    assert plan(4096, tune=N.Tune(tail_rows=-1))["tail"] == 0 and plan(4096)["tail"] > 0
+    tail = plan(4096, tune=N.Tune(tail_rows=-1))
+    assert tail["seg"] == plan(4096)["seg"]
 
 
 @pytest.mark.parametrize("n", [512, 1024, 1448, 2048])
