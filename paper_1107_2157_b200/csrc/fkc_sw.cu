@@ -17,6 +17,13 @@
 #include "sw_tma.cuh"
 #include "sw_resident.cuh"
 
+#ifndef FKC_GEN_BX
+#define FKC_GEN_BX 64              // generic kernel CTA: 64 x 4 cells
+#endif
+#ifndef FKC_GEN_BY
+#define FKC_GEN_BY 4
+#endif
+
 using namespace fkc;
 
 namespace {
@@ -247,8 +254,8 @@ int launch_generic(const fkc_sw_step_args* a, cudaStream_t st) {
     const fkc_grid& g = a->grid;
     DtSrc dts{a->dt, (const unsigned long long*)a->dt_bound, a->cfl};
     RedPtrs red = to_red(a->red);
-    dim3 blk(64, 4);
-    dim3 grd((g.nx + 63) / 64, (g.ny + 3) / 4);
+    dim3 blk(FKC_GEN_BX, FKC_GEN_BY);
+    dim3 grd((g.nx + FKC_GEN_BX - 1) / FKC_GEN_BX, (g.ny + FKC_GEN_BY - 1) / FKC_GEN_BY);
     const bool fast = a->mode == FKC_MODE_FAST;
     const bool r = any_red(red);
     const bool pdl = !a->tune.no_pdl && (int64_t)g.nx * g.ny >= (1 << 18) &&
